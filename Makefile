@@ -1,0 +1,43 @@
+# Top-level build: every native artefact of the repo (run by __graft_entry__.build()).
+#   paper_1905_04341_b200/lib/libpmhd_host.so        host C++ layer (pmhd_host.h)
+#   paper_1905_04341_b200/lib/libpmhd_gpu.so         CUDA C-ABI, sm_100a, FMA build (product)
+#   paper_1905_04341_b200/lib/libpmhd_gpu_parity.so  same sources, --fmad=false (bitwise parity runs)
+#   paper_1905_04341_b200/bin/pmhd                   C++ CLI (run / bench) over the two libraries
+#   oracle/liboracle.so (+ oracle/_ref/)             CPU oracle -- test infrastructure
+NVCC     ?= nvcc
+HOSTCXX  ?= g++
+PKG      := paper_1905_04341_b200
+LIB      := $(PKG)/lib
+GPUSRC   := $(PKG)/csrc/gpu
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -Xlinker -Bsymbolic -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Iinclude -I$(GPUSRC) \
+            -Xptxas -warn-spills --expt-relaxed-constexpr
+HOSTFLAGS:= -std=c++20 -O2 -march=x86-64-v3 -fPIC -Wall -Wextra -Iinclude
+GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu
+GPU_DEPS := $(GPU_SRCS) $(wildcard $(GPUSRC)/*.cuh) include/pmhd_gpu.h
+
+all: host gpu oracle
+
+host: $(LIB)/libpmhd_host.so
+gpu: $(LIB)/libpmhd_gpu.so $(LIB)/libpmhd_gpu_parity.so
+
+$(LIB)/libpmhd_host.so: $(PKG)/csrc/host/pmhd_host.cpp include/pmhd_host.h include/pmhd_gpu.h
+	@mkdir -p $(LIB)
+	$(HOSTCXX) $(HOSTFLAGS) -shared -o $@ $<
+
+$(LIB)/libpmhd_gpu.so: $(GPU_DEPS)
+	@mkdir -p $(LIB)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPU_SRCS)
+
+$(LIB)/libpmhd_gpu_parity.so: $(GPU_DEPS)
+	@mkdir -p $(LIB)
+	$(NVCC) $(NVFLAGS) --fmad=false -DPMHD_PARITY -shared -o $@ $(GPU_SRCS)
+
+oracle:
+	$(MAKE) -C oracle CXX=$(HOSTCXX)
+
+clean:
+	rm -f $(LIB)/*.so
+	$(MAKE) -C oracle clean
+
+.PHONY: all host gpu oracle clean

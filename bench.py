@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""bench.py -- fp64 VL2+PLM+HLLD+CT MHD throughput on B200 (cell-updates/s).
+
+Workload (BASELINE.json config 4 at N=1): 3D linear fast
+magnetosonic wave, 256^3 active cells in ONE MeshBlock per GPU, ng=2,
+gamma=5/3, CFL 0.3, A=1e-6 along x1, HLLD + PLM(MC) + contact-upwind CT.
+A "step" is one full VL2 cycle (stage 1 + stage 2 + exchanges + dt).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N>1) each rank owns one 256^3 block of a (256 N) x 256 x 256
+periodic mesh (weak scaling); dt is all-reduced (min) over ranks every cycle.
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_ALG = 320.0          # compulsory HBM bytes per cell-update
+F_ALG_FILE = os.path.join(ROOT, "profiles", "falg_counting.json")
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=256, help="cells per dimension per GPU")
+    p.add_argument("--riemann", default="hlld")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_config(n, ranks, riemann="hlld", nz=None):
+    from paper_1905_04341_b200 import RunConfig
+    nz = n if nz is None else nz
+    return RunConfig(nx1=n * ranks, nx2=n, nx3=nz, mb1=n, mb2=n, mb3=nz, x1max=float(ranks),
+                     x3max=nz / n, wave_mode=6, wave_amp=1e-6, cfl=0.3, riemann=riemann)
+
+
+def falg():
+    try:
+        d = json.load(open(F_ALG_FILE))
+        return float(d["256"]["per_cell_update"]), "oracle CountingScalar at 256^3 (profiles/falg_counting.json)"
+    except Exception:
+        return 2790.0, "estimate"
+
+
+def fp64_peak():
+    try:
+        d = json.load(open(FP64_PEAK_FILE))
+        return float(d["fp64_dfma_tflops"]), "measured (profiles/fp64_peak.json, tools/fp64_peak.cu)"
+    except Exception:
+        return 37.2, "nominal (148 SM x 64 DFMA x 2 x 1.965 GHz)"
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(PEAKS_FILE))["hbm_gbs"]), "of measured"
+    except Exception:
+        return 6650.0, "of fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nme, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nme)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_oracle_cups(n, cycles_max, seconds, workers, nz=32):
+    """The oracle (test infrastructure) on a bounded sample of the workload:
+    the 256 x 256 x nz periodic slab of the M4 linear wave (same per-cell
+    work).  Dispatched through the reference's own par_for / ThreadPool
+    (oracle/_ref) when that build is present."""
+    from oracle.binding import OracleSolver
+    ref = os.path.exists(os.path.join(ROOT, "oracle", "_ref", "liboracle_ref.so"))
+    cfg = make_config(n, 1, nz=nz)
+    s = OracleSolver(cfg, workers=workers, ref=ref)
+    s.load_pgen()
+    dt = s.new_dt()
+    dt, _ = s.vl2_step(dt)  # warm-up (page faults)
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < cycles_max:
+        t0 = time.perf_counter()
+        dt, _ = s.vl2_step(dt)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > seconds:
+            break
+    cells = cfg.active_cells
+    per = [cells / t for t in times]
+    return {"value": cells * len(times) / sum(times), "p80": sorted(per)[int(0.8 * (len(per) - 1))],
+            "unit": "cell-updates/s", "cores": workers, "kind": "port",
+            "sample": f"{len(times)} VL2 cycle(s) of the {n}x{n}x{nz} periodic slab of the M4 linear wave "
+                      f"(same per-cell work as 256^3), oracle/{'_ref (reference par_for/ThreadPool, SimdNested)' if ref else 'liboracle.so'}, "
+                      f"{workers} worker threads"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    from oracle.binding import OracleSolver
+    ref = os.path.exists(os.path.join(ROOT, "oracle", "_ref", "liboracle_ref.so"))
+    nz = 32
+    cfg = make_config(args.n, 1, riemann=args.riemann, nz=nz)
+    s = OracleSolver(cfg, workers=workers, ref=ref)
+    s.load_pgen()
+    dt = s.new_dt()
+    for _ in range(args.warmup):
+        dt, _ = s.vl2_step(dt)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        dt, _ = s.vl2_step(dt)
+        times.append(time.perf_counter() - t0)
+    cells = cfg.active_cells
+    tot = sum(times)
+    value = cells * len(times) / tot
+    sample = (f"each step = 1 VL2 cycle of the {args.n}x{args.n}x{nz} periodic slab of the M4 linear wave "
+              f"(bounded sample of the 256^3 workload; identical per-cell work), CPU oracle "
+              f"{'through the reference par_for/ThreadPool (oracle/_ref)' if ref else '(oracle/liboracle.so)'}")
+    line = {"impl": "reference", "metric": "cell-updates/s (fp64 VL2+PLM+HLLD+CT MHD)", "value": value,
+            "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (linear-wave problem generator)",
+            "config": {"workload": f"M4 linear fast wave {args.n}^3 per GPU (sampled as {args.n}x{args.n}x{nz})",
+                       "riemann": args.riemann, "cells_per_step": cells},
+            "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": workers, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import numpy as np
+    import torch
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_1905_04341_b200.solver import GpuSolver
+    from paper_1905_04341_b200 import native as N
+
+    n = args.n
+    cfg = make_config(n, 1, riemann=args.riemann)  # this rank's periodic 256^3 block
+    cells_rank = cfg.active_cells
+    g = GpuSolver(cfg, device=local)
+    stream = torch.cuda.ExternalStream(g.stream_handle, device=torch.device("cuda", local))
+    host = cfg.pgen_block(0)
+    g.set_block(0, host)
+    g.exchange()
+    dt = g.new_dt()
+
+    def allreduce_min(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return float(t.item())
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    dt = allreduce_min(dt)
+    for _ in range(args.warmup):
+        dt, _ = g.vl2_step(dt)
+        dt = allreduce_min(dt)
+    # ---- timed region (inputs resident in HBM, 1.5 GB state >> 126 MB L2) ----
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    g.region_times(reset=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        evs[0].record(stream)
+        for k in range(args.steps):
+            dt, _ = g.vl2_step(dt)
+            dt = allreduce_min(dt)
+            evs[k + 1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = g.region_times()["kernel_launches"]
+    per_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    tot_ms = evs[0].elapsed_time(evs[-1])
+    if dist is not None:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = ws * cells_rank * args.steps / (tot_ms * 1e-3)
+    per_cups = sorted(cells_rank * ws / (m * 1e-3) for m in per_ms)
+    p80 = per_cups[int(0.8 * (len(per_cups) - 1))]
+
+    # ---- profiled pass (region events) for the roofline ----
+    g.set_profiling(True)
+    g.region_times(reset=True)
+    nprof = max(2, min(args.steps, 4))
+    for _ in range(nprof):
+        dt, _ = g.vl2_step(dt)
+        dt = allreduce_min(dt)
+    rt = g.region_times(reset=True)
+    g.set_profiling(False)
+    kern_ms = (rt["c2p_ms"] + rt["riemann_ms"] + rt["ct_emf_ms"] + rt["integrate_ms"] +
+               rt["boundary_ms"]) / nprof
+    F_alg, F_src = falg()
+    fp64_pk, fp64_src = fp64_peak()
+    hbm_pk, hbm_src = hbm_peak()
+    cycle_ms_kernels = kern_ms
+    ach_gbs = B_ALG * cells_rank / (cycle_ms_kernels * 1e-3) / 1e9
+    ach_tf = F_alg * cells_rank / (cycle_ms_kernels * 1e-3) / 1e12
+    shares = {k: rt[k] / max(1e-9, kern_ms * nprof) for k in
+              ("c2p_ms", "riemann_ms", "ct_emf_ms", "integrate_ms", "boundary_ms")}
+    roofline = {
+        "bound": "hbm", "achieved": ach_gbs, "peak": hbm_pk, "unit": "GB/s", "frac": ach_gbs / hbm_pk,
+        "traffic": None, "peak_source": hbm_src,
+        "kernel": "whole VL2 cycle (all stage kernels; B_alg = 320 B/cell-update, SURVEY.md §8d)",
+        "fp64": {"achieved": ach_tf, "peak": fp64_pk, "unit": "TFLOP/s", "frac": ach_tf / fp64_pk,
+                 "F_alg_per_cell_update": F_alg, "F_alg_source": F_src, "peak_source": fp64_src},
+        "binding_ceiling": "fp64" if F_alg / fp64_pk > B_ALG / (hbm_pk / 1e3) else "hbm",
+        # paper Eq. 2 against the binding ceiling (SURVEY.md §8d judged figure)
+        "roofline_achieved_eq2": (cells_rank / (cycle_ms_kernels * 1e-3)) /
+        min(hbm_pk * 1e9 / B_ALG, fp64_pk * 1e12 / F_alg),
+        "region_share": shares,
+        "dominant_region": max(shares, key=shares.get),
+    }
+
+    # ---- e2e through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        cudart = torch.cuda.cudart()
+        arrs = [host.u, host.b1f, host.b2f, host.b3f]
+        out = cfg.new_block()
+        outs = [out.u, out.b1f, out.b2f, out.b3f]
+        for a in arrs + outs:
+            cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+        h2d = host.u[:5].nbytes + host.b1f.nbytes + host.b2f.nbytes + host.b3f.nbytes
+        d2h = out.u[:5].nbytes + out.b1f.nbytes + out.b2f.nbytes + out.b3f.nbytes
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.set_block(0, host)
+        g.exchange()
+        d = allreduce_min(g.new_dt())
+        for _ in range(args.steps):
+            d, _ = g.vl2_step(d)
+            d = allreduce_min(d)
+        out = g.get_block(0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        for a in arrs + outs:
+            cudart.cudaHostUnregister(a.ctypes.data)
+        e2e = {"value": ws * cells_rank * args.steps / (ms * 1e-3), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+               "how": "pmhd_gpu_upload_block (pinned host) + exchange + new_dt + K x pmhd_gpu_vl2_step + "
+                      "pmhd_gpu_download_block, one CUDA-event region on the ABI stream; the whole "
+                      "block state crosses PCIe once each way per K steps"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_cups(n, 5, args.cpu_seconds, os.cpu_count() or 1)
+
+    if rank == 0:
+        line = {
+            "metric": "cell-updates/s (fp64 VL2+PLM+HLLD+CT MHD)", "value": value,
+            "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (linear-wave problem generator)",
+            "config": {"workload": f"M4 3D linear fast wave, {n}^3 active cells per GPU in one MeshBlock, "
+                                   f"HLLD+PLM(MC)+CT, CFL 0.3, A=1e-6",
+                       "global_cells": [n * ws, n, n], "parallelism": f"{ws} rank(s), one 256^3 block each",
+                       "l2": "inputs larger than L2 (1.5 GB state per GPU vs 126 MB L2)",
+                       "statistic": "value = mean over K cycles; p80 in extra.p80_cups",
+                       "variant": g.build_info},
+            "p80_cups": p80,
+            "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    g.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

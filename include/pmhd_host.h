@@ -1,0 +1,103 @@
+/*
+ * pmhd_host.h -- C API of the host-side C++ library (libpmhd_host.so):
+ * input-file parsing, MeshConfig/MeshBlock geometry and the problem
+ * generators.  This is the host layer that sits above the GPU C-ABI
+ * (pmhd_gpu.h); the reference defines it in
+ *   parse_config
+ *   MeshConfig/build_mesh
+ *   init_linear_wave    SPEC.md:218-226   (WaveSetup SPEC.md:126-129)
+ *   l1_error
+ * plus the Orszag-Tang, blast and turbulence generators that BASELINE.json's
+ * configs require (definitions in DESIGN.md / SURVEY.md §8d).
+ */
+#ifndef PMHD_HOST_H_
+#define PMHD_HOST_H_
+
+#include <stdint.h>
+
+#include "pmhd_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PMHD_PGEN_LINEAR_WAVE = 0,
+  PMHD_PGEN_ORSZAG_TANG = 1,
+  PMHD_PGEN_BLAST = 2,
+  PMHD_PGEN_TURBULENCE = 3,
+  PMHD_PGEN_UNIFORM = 4
+};
+
+/* Linear-wave eigenmodes, ordered by eigenvalue (Athena++ wave_flag order):
+ * 0 fast-left, 1 Alfven-left, 2 slow-left, 3 entropy, 4 slow-right,
+ * 5 Alfven-right, 6 fast-right. */
+
+/* RunConfig. */
+typedef struct pmhd_run_config {
+  pmhd_mesh_desc mesh;
+  int pgen;                 /* PMHD_PGEN_*                                      */
+  /* WaveSetup; background in the wave frame (n,t1,t2)    */
+  double wave_amp;          /* A, default 1e-6                                  */
+  int wave_n[3];            /* integer periods per domain, default (1,0,0)     */
+  int wave_mode;            /* 0..6, default 6 (fast, right-going)              */
+  double wave_rho, wave_p;  /* default 1, 0.6                                   */
+  double wave_v[3];         /* (vn, vt1, vt2), default 0                        */
+  double wave_b[3];         /* (bn, bt1, bt2), default (1, sqrt 2, 0.5)         */
+  /* blast */
+  double blast_pin, blast_pout, blast_r, blast_rho;
+  double blast_b[3];
+  /* turbulence */
+  double turb_mach;
+  uint64_t turb_seed;
+  /* uniform state (pgen uniform): rho, v1..3, p, B1..3 */
+  double uniform_w[8];
+  /* run control */
+  int nlim;                 /* cycle limit (-1: none)                           */
+  double tlim;              /* time limit (<= 0: one wave period / pgen default) */
+  int workers;              /* CPU workers (oracle / baseline)                  */
+  int gpus;
+} pmhd_run_config;
+
+/* Defaults (empty text -> 16^3, one block). */
+void pmhd_host_config_defaults(pmhd_run_config* cfg);
+
+/* parse_config: "key = value" lines, '#' comments, later
+ * keys override, unknown key or malformed value -> PMHD_ERR_INPUT with
+ * *err_line set (1-based) and a message in err (may be NULL). */
+int pmhd_host_config_parse(const char* text, pmhd_run_config* cfg, int* err_line, char* err,
+                           int errlen);
+
+/* MeshConfig invariants -> PMHD_ERR_CONFIG. */
+int pmhd_host_validate(const pmhd_run_config* cfg, char* err, int errlen);
+
+/* Block geometry: number of blocks, array extents (with ghosts), cell sizes. */
+int pmhd_host_nblocks(const pmhd_run_config* cfg);
+void pmhd_host_block_dims(const pmhd_run_config* cfg, int n[3]);
+void pmhd_host_block_coords(const pmhd_run_config* cfg, int gid, int c[3]);
+
+/* Problem generator: fills the ACTIVE cells and faces of block gid (ghosts are
+ * left untouched; call exchange afterwards).  u: 8 vars (Bcc from the face
+ * average), faces as in pmhd_gpu.h. */
+int pmhd_host_pgen_block(const pmhd_run_config* cfg, int gid, double* u, double* b1f,
+                         double* b2f, double* b3f);
+
+/* Exact linear-wave solution at time t at the cell centres of the active
+ * cells of block gid: 8 vars (rho, m1, m2, m3, E, B1, B2, B3), NCONS x n3 x
+ * n2 x n1 layout (ghost entries untouched). */
+int pmhd_host_exact_block(const pmhd_run_config* cfg, int gid, double t, double* u);
+
+/* Linear-wave eigen data: eigenvalue (phase speed along n) of the selected
+ * mode, right eigenvector (7 conserved wave-frame components), and the
+ * residual ||(J - lambda I) r||_inf of the complex-step flux Jacobian. */
+int pmhd_host_wave_eigen(const pmhd_run_config* cfg, double* lambda, double r[7],
+                         double* residual);
+
+/* Default end time of the problem (one wave period for linear waves). */
+double pmhd_host_default_tlim(const pmhd_run_config* cfg);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMHD_HOST_H_ */

@@ -1,0 +1,71 @@
+// kernels.cuh -- device data layout shared by the ABI and the kernels.
+//
+// HBM layout: every per-block field is a dense
+// k-j-i array (i fastest, the reference's Array3 order, array.hpp:30-35) with
+// a padded row pitch sx (multiple of 32 doubles = 256 B) and a plane pitch
+// sy = sx * (n2 + 1), so cell-, face- and edge-centred arrays share one index
+// function idx(k,j,i) = k*sy + j*sx + i.  Variables are separate arrays
+// (variable-major, array.hpp:61-66).
+#ifndef PMHD_KERNELS_CUH_
+#define PMHD_KERNELS_CUH_
+
+#include <cuda_runtime.h>
+
+#include "physics.cuh"
+
+namespace pmhd_gpu {
+
+constexpr int kNState = 8;  // u0..u4 (rho, m1, m2, m3, E), b1f, b2f, b3f
+
+struct KGeom {
+  int n1, n2, n3;     // cell extents incl. ghosts
+  long long sx, sy;   // row / plane pitch (doubles)
+  int is, ie, js, je, ks, ke;
+  int dim, nb, ng;
+  int nx[3], mb[3];
+  double dx[3];
+  __host__ __device__ long long idx(int k, int j, int i) const { return k * sy + j * sx + i; }
+};
+
+struct DevBlock {
+  double* st[2][kNState];  // state A (0) and B (1)
+  double* w[8];            // stage-input primitives incl. Bcc (split kernels)
+  double* fx[3][8];        // face data: 5 lab-order fluxes, ey, ez, weight
+  double* e[3];            // corner EMFs e1, e2, e3
+  int c[3];                // block coordinates
+  int nbr[3][2];           // local index of the lower / upper neighbour
+};
+
+// Device-side reduction slots: red[0] = init / dt, red[1..2] = stage 1..2.
+struct DevRed {
+  unsigned long long dt_bits;     // min over cells of dx/(|v|+cf), as bits
+  unsigned long long bad_key;     // smallest failing global cell key
+  unsigned long long floor_count;
+  unsigned long long divb_bits;   // max |div B| as bits
+};
+
+// Stage coefficients c_d = beta*dt/dx_d, computed on the host with the same
+// IEEE operations as the oracle.
+struct KStage {
+  double c1, c2, c3;
+  int in_sel, out_sel, stage, plm;
+};
+
+// Launchers (kernels.cu).
+void launch_c2p_all(const DevBlock* blks, const KGeom& G, const KPhys& ph, int sel, DevRed* red,
+                    int stage, cudaStream_t s);
+void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel, int plm,
+                 cudaStream_t s);
+void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s);
+void launch_update(const DevBlock* blks, const KGeom& G, const KStage& ks, cudaStream_t s);
+void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
+                    DevRed* red, int want_dt, cudaStream_t s);
+void launch_exchange(const DevBlock* blks, const KGeom& G, int sel, cudaStream_t s);
+void launch_dt_from_state(const DevBlock* blks, const KGeom& G, const KPhys& ph, DevRed* red,
+                          cudaStream_t s);
+void launch_divb(const DevBlock* blks, const KGeom& G, DevRed* red, cudaStream_t s);
+void launch_row_sums(const DevBlock* blks, const KGeom& G, double* rows, cudaStream_t s);
+
+}  // namespace pmhd_gpu
+
+#endif

@@ -1,0 +1,574 @@
+// pmhd_gpu.cu -- implementation of the C ABI (include/pmhd_gpu.h).
+//
+// Owns all device memory through opaque handles; host pointers are borrowed
+// for the duration of a call.  Each call returns once its results are visible
+// to the next call (the par_for synchronization-point contract,
+// /root/reference/proj/include/pmhd/exec/dispatch.hpp:106-108).  No C++
+// exception crosses the ABI; errors map to the defs.hpp:36-76 families.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "pmhd_gpu.h"
+
+using namespace pmhd_gpu;
+
+#ifndef PMHD_VARIANT
+#define PMHD_VARIANT "split"
+#endif
+#ifdef PMHD_PARITY
+#define PMHD_BUILD_INFO PMHD_VARIANT "+parity(fmad=false)"
+#else
+#define PMHD_BUILD_INFO PMHD_VARIANT "+fma"
+#endif
+
+struct pmhd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+};
+
+struct pmhd_mesh {
+  pmhd_ctx* ctx = nullptr;
+  pmhd_mesh_desc desc;
+  KGeom G;
+  KPhys ph;
+  std::vector<int> gids;          // global id of each local block
+  std::vector<DevBlock> hblk;
+  DevBlock* dblk = nullptr;
+  double* slab = nullptr;
+  size_t arr_elems = 0;
+  DevRed* dred = nullptr;         // 3 slots
+  DevRed* hred = nullptr;         // pinned mirror
+  double* drows = nullptr;
+  bool all_local = true;
+  bool prof = false;
+  cudaEvent_t ev[8] = {};
+  pmhd_region_times times{};
+};
+
+namespace {
+
+#define CK(call)                                                               \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);          \
+      return PMHD_ERR_CUDA;                                                    \
+    }                                                                          \
+  } while (0)
+
+int fail(pmhd_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+std::string validate(const pmhd_mesh_desc& d) {
+  if (d.ng < 2) return "ng must be >= 2";
+  for (int a = 0; a < 3; ++a) {
+    if (d.nx[a] < 1 || d.mb[a] < 1) return "cell counts must be positive";
+    if (d.nx[a] % d.mb[a] != 0) return "global cells not divisible by meshblock cells";
+    if (!(d.xmax[a] > d.xmin[a])) return "empty domain extent";
+  }
+  if (d.nx[1] == 1) return "1D meshes are not supported";
+  if (d.mb[0] <= d.ng || d.mb[1] <= d.ng || (d.nx[2] > 1 && d.mb[2] <= d.ng))
+    return "meshblock must have more than ng cells per dimension";
+  if (!(d.gamma > 1.0)) return "gamma must be > 1";
+  if (!(d.cfl > 0.0 && d.cfl < 1.0)) return "cfl must be in (0,1)";
+  if (d.riemann != PMHD_RIEMANN_HLLD && d.riemann != PMHD_RIEMANN_HLLE) return "bad riemann";
+  if (d.limiter != PMHD_LIMITER_MC && d.limiter != PMHD_LIMITER_VANLEER) return "bad limiter";
+  if (d.eos_mode != PMHD_EOS_ERROR && d.eos_mode != PMHD_EOS_FLOOR) return "bad eos_mode";
+  if (d.emf_mode != PMHD_EMF_UPWIND && d.emf_mode != PMHD_EMF_ARITH) return "bad emf_mode";
+  return "";
+}
+
+void decode_key(const KGeom& G, unsigned long long key, pmhd_status* st) {
+  st->i = int(key % (unsigned long long)G.nx[0]);
+  st->j = int((key / (unsigned long long)G.nx[0]) % (unsigned long long)G.nx[1]);
+  st->k = int(key / (unsigned long long)G.nx[0] / (unsigned long long)G.nx[1]);
+}
+
+double bits2d(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, sizeof(d));
+  return d;
+}
+
+int reset_red(pmhd_mesh* m) {
+  pmhd_ctx* ctx = m->ctx;
+  for (int s = 0; s < 3; ++s) {
+    m->hred[s].dt_bits = 0x7FF0000000000000ULL;  // +inf
+    m->hred[s].bad_key = ULLONG_MAX;
+    m->hred[s].floor_count = 0;
+    m->hred[s].divb_bits = 0;
+  }
+  CK(cudaMemcpyAsync(m->dred, m->hred, 3 * sizeof(DevRed), cudaMemcpyHostToDevice, ctx->stream));
+  return PMHD_OK;
+}
+
+int fetch_red(pmhd_mesh* m) {
+  pmhd_ctx* ctx = m->ctx;
+  CK(cudaMemcpyAsync(m->hred, m->dred, 3 * sizeof(DevRed), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  return PMHD_OK;
+}
+
+void rec(pmhd_mesh* m, int slot) {
+  if (m->prof) cudaEventRecord(m->ev[slot], m->ctx->stream);
+}
+
+// Enqueue one VL2 stage (no synchronization unless profiling).
+int enqueue_stage(pmhd_mesh* m, int s, double dt) {
+  pmhd_ctx* ctx = m->ctx;
+  const KGeom& G = m->G;
+  const double beta = (s == 1) ? 0.5 : 1.0;
+  const double bdt = beta * dt;
+  KStage ks;
+  ks.c1 = bdt / G.dx[0];
+  ks.c2 = bdt / G.dx[1];
+  ks.c3 = bdt / G.dx[2];
+  ks.in_sel = (s == 1) ? 0 : 1;
+  ks.out_sel = (s == 1) ? 1 : 0;
+  ks.stage = s;
+  ks.plm = (s == 2);
+  cudaStream_t st = ctx->stream;
+  rec(m, 0);
+  launch_c2p_all(m->dblk, G, m->ph, ks.in_sel, m->dred, s, st);
+  rec(m, 1);
+  for (int dir = 0; dir < G.dim; ++dir) launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, st);
+  rec(m, 2);
+  launch_emf(m->dblk, G, m->ph, st);
+  rec(m, 3);
+  launch_update(m->dblk, G, ks, st);
+  launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
+  rec(m, 4);
+  launch_exchange(m->dblk, G, ks.out_sel, st);
+  rec(m, 5);
+  m->times.kernel_launches += 4 + 2 * G.dim;
+  CK(cudaGetLastError());
+  if (m->prof) {
+    CK(cudaEventSynchronize(m->ev[5]));
+    float t[5];
+    for (int q = 0; q < 5; ++q) cudaEventElapsedTime(&t[q], m->ev[q], m->ev[q + 1]);
+    m->times.c2p_ms += t[0];
+    m->times.riemann_ms += t[1];
+    m->times.ct_emf_ms += t[2];
+    m->times.integrate_ms += t[3];
+    m->times.boundary_ms += t[4];
+    m->times.calls += 1;
+  }
+  return PMHD_OK;
+}
+
+int finish(pmhd_mesh* m, int stage_lo, int stage_hi, double* dt_next, pmhd_status* st) {
+  int rc = fetch_red(m);
+  if (rc) return rc;
+  pmhd_status s{};
+  s.code = PMHD_OK;
+  s.k = s.j = s.i = -1;
+  s.stage = stage_hi;
+  long long nf = 0;
+  for (int q = stage_lo; q <= stage_hi; ++q) nf += (long long)m->hred[q].floor_count;
+  s.floor_count = nf;
+  for (int q = stage_lo; q <= stage_hi; ++q) {
+    if (m->hred[q].bad_key != ULLONG_MAX) {
+      s.code = PMHD_ERR_UNPHYSICAL;
+      s.stage = q;
+      decode_key(m->G, m->hred[q].bad_key, &s);
+      break;
+    }
+  }
+  if (dt_next) *dt_next = m->desc.cfl * bits2d(m->hred[0].dt_bits);
+  if (st) *st = s;
+  if (s.code != PMHD_OK) {
+    m->ctx->err = "unphysical state in stage " + std::to_string(s.stage);
+    return PMHD_ERR_UNPHYSICAL;
+  }
+  return PMHD_OK;
+}
+
+int copy3d(pmhd_ctx* ctx, void* dst, size_t dpitch, size_t dy, const void* src, size_t spitch,
+           size_t sy, size_t wbytes, size_t h, size_t d, cudaMemcpyKind kind) {
+  cudaMemcpy3DParms p;
+  std::memset(&p, 0, sizeof(p));
+  p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), spitch, wbytes / sizeof(double), sy);
+  p.dstPtr = make_cudaPitchedPtr(dst, dpitch, wbytes / sizeof(double), dy);
+  p.extent = make_cudaExtent(wbytes, h, d);
+  p.kind = kind;
+  CK(cudaMemcpy3DAsync(&p, ctx->stream));
+  return PMHD_OK;
+}
+
+int local_index(const pmhd_mesh* m, int gid) {
+  for (size_t b = 0; b < m->gids.size(); ++b)
+    if (m->gids[b] == gid) return int(b);
+  return -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pmhd_gpu_abi_version(void) { return PMHD_ABI_VERSION; }
+
+const char* pmhd_gpu_build_info(void) { return PMHD_BUILD_INFO; }
+
+int pmhd_gpu_ctx_create(int device, pmhd_ctx** out) {
+  if (!out) return PMHD_ERR_INPUT;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) return PMHD_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return PMHD_ERR_CUDA;
+  if (prop.major != 10) return PMHD_ERR_CUDA;  // built for sm_100a only
+  auto* ctx = new pmhd_ctx;
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return PMHD_ERR_CUDA;
+  }
+  *out = ctx;
+  return PMHD_OK;
+}
+
+int pmhd_gpu_ctx_destroy(pmhd_ctx* ctx) {
+  if (!ctx) return PMHD_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return PMHD_OK;
+}
+
+const char* pmhd_gpu_last_error(const pmhd_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* gids, int n_local,
+                         pmhd_mesh** out) {
+  if (!ctx || !desc || !out) return PMHD_ERR_INPUT;
+  *out = nullptr;
+  const std::string v = validate(*desc);
+  if (!v.empty()) return fail(ctx, PMHD_ERR_CONFIG, v);
+  CK(cudaSetDevice(ctx->device));
+  auto* m = new pmhd_mesh;
+  m->ctx = ctx;
+  m->desc = *desc;
+  KGeom& G = m->G;
+  G.dim = (desc->nx[2] == 1) ? 2 : 3;
+  G.ng = desc->ng;
+  int nb[3];
+  for (int a = 0; a < 3; ++a) {
+    G.nx[a] = desc->nx[a];
+    G.mb[a] = desc->mb[a];
+    nb[a] = desc->nx[a] / desc->mb[a];
+    G.dx[a] = (desc->xmax[a] - desc->xmin[a]) / desc->nx[a];
+  }
+  G.n1 = G.mb[0] + 2 * G.ng;
+  G.n2 = G.mb[1] + 2 * G.ng;
+  G.n3 = (G.dim == 3) ? G.mb[2] + 2 * G.ng : 1;
+  G.sx = ((G.n1 + 1 + 31) / 32) * 32;
+  G.sy = G.sx * (G.n2 + 1);
+  G.is = G.ng; G.ie = G.ng + G.mb[0];
+  G.js = G.ng; G.je = G.ng + G.mb[1];
+  if (G.dim == 3) { G.ks = G.ng; G.ke = G.ng + G.mb[2]; } else { G.ks = 0; G.ke = 1; }
+  const int ntot = nb[0] * nb[1] * nb[2];
+  if (n_local <= 0 || !gids) {
+    for (int g = 0; g < ntot; ++g) m->gids.push_back(g);
+  } else {
+    for (int b = 0; b < n_local; ++b) {
+      if (gids[b] < 0 || gids[b] >= ntot) { delete m; return fail(ctx, PMHD_ERR_CONFIG, "gid out of range"); }
+      m->gids.push_back(gids[b]);
+    }
+  }
+  G.nb = int(m->gids.size());
+  m->ph.gamma = desc->gamma;
+  m->ph.gm1 = desc->gamma - 1.0;
+  m->ph.igm1 = 1.0 / (desc->gamma - 1.0);
+  m->ph.dfloor = desc->dfloor;
+  m->ph.pfloor = desc->pfloor;
+  m->ph.riemann = desc->riemann;
+  m->ph.limiter = desc->limiter;
+  m->ph.eos = desc->eos_mode;
+  m->ph.emf = desc->emf_mode;
+
+  // one slab: 51 arrays per block, each (n3+1)*sy doubles plus a 64-double guard
+  const size_t arr = size_t(G.n3 + 1) * size_t(G.sy) + 64;
+  m->arr_elems = arr;
+  const size_t per_block = 51 * arr;
+  const size_t bytes = per_block * G.nb * sizeof(double);
+  if (cudaMalloc(&m->slab, bytes) != cudaSuccess) {
+    delete m;
+    return fail(ctx, PMHD_ERR_CUDA, "device allocation of " + std::to_string(bytes) + " bytes failed");
+  }
+  cudaMemsetAsync(m->slab, 0, bytes, ctx->stream);
+  m->hblk.resize(G.nb);
+  for (int b = 0; b < G.nb; ++b) {
+    double* p = m->slab + size_t(b) * per_block + 32;
+    DevBlock& B = m->hblk[b];
+    auto take = [&]() { double* q = p; p += arr; return q; };
+    for (int s = 0; s < 2; ++s)
+      for (int v = 0; v < kNState; ++v) B.st[s][v] = take();
+    for (int v = 0; v < 8; ++v) B.w[v] = take();
+    for (int d = 0; d < 3; ++d)
+      for (int v = 0; v < 8; ++v) B.fx[d][v] = take();
+    for (int c = 0; c < 3; ++c) B.e[c] = take();
+    const int gid = m->gids[b];
+    B.c[0] = gid % nb[0];
+    B.c[1] = (gid / nb[0]) % nb[1];
+    B.c[2] = gid / (nb[0] * nb[1]);
+    for (int d = 0; d < 3; ++d)
+      for (int side = 0; side < 2; ++side) {
+        int c[3] = {B.c[0], B.c[1], B.c[2]};
+        c[d] = (c[d] + (side ? 1 : -1) + nb[d]) % nb[d];
+        const int ng = (c[2] * nb[1] + c[1]) * nb[0] + c[0];
+        int li = -1;
+        for (int q = 0; q < G.nb; ++q) if (m->gids[q] == ng) { li = q; break; }
+        if (li < 0) { m->all_local = false; li = b; }
+        B.nbr[d][side] = li;
+      }
+  }
+  CK(cudaMalloc(&m->dblk, sizeof(DevBlock) * G.nb));
+  CK(cudaMemcpyAsync(m->dblk, m->hblk.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMalloc(&m->dred, 3 * sizeof(DevRed)));
+  CK(cudaMallocHost(&m->hred, 3 * sizeof(DevRed)));
+  const size_t nrows = size_t(G.nb) * 5 * (G.ke - G.ks) * (G.je - G.js);
+  CK(cudaMalloc(&m->drows, nrows * sizeof(double)));
+  for (auto& e : m->ev) CK(cudaEventCreate(&e));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *out = m;
+  return PMHD_OK;
+}
+
+int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
+  if (!m) return PMHD_OK;
+  cudaSetDevice(m->ctx->device);
+  cudaStreamSynchronize(m->ctx->stream);
+  cudaFree(m->slab);
+  cudaFree(m->dblk);
+  cudaFree(m->dred);
+  cudaFree(m->drows);
+  cudaFreeHost(m->hred);
+  for (auto& e : m->ev) if (e) cudaEventDestroy(e);
+  delete m;
+  return PMHD_OK;
+}
+
+int pmhd_gpu_block_dims(const pmhd_mesh* m, int n[3]) {
+  if (!m || !n) return PMHD_ERR_INPUT;
+  n[0] = m->G.n1; n[1] = m->G.n2; n[2] = m->G.n3;
+  return PMHD_OK;
+}
+
+int pmhd_gpu_upload_block(pmhd_mesh* m, int gid, const double* u, const double* b1f,
+                          const double* b2f, const double* b3f) {
+  if (!m) return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  const int b = local_index(m, gid);
+  if (b < 0) return fail(ctx, PMHD_ERR_INPUT, "block not local");
+  if (!u || !b1f || !b2f || !b3f) return fail(ctx, PMHD_ERR_BUFFER, "null buffer");
+  const KGeom& G = m->G;
+  const size_t dp = size_t(G.sx) * sizeof(double), dy = size_t(G.n2 + 1);
+  const size_t nc = size_t(G.n1) * G.n2 * G.n3;
+  DevBlock& B = m->hblk[b];
+  for (int v = 0; v < 5; ++v) {
+    int rc = copy3d(ctx, B.st[0][v], dp, dy, u + v * nc, G.n1 * sizeof(double), G.n2,
+                    G.n1 * sizeof(double), G.n2, G.n3, cudaMemcpyHostToDevice);
+    if (rc) return rc;
+  }
+  int rc = copy3d(ctx, B.st[0][5], dp, dy, b1f, (G.n1 + 1) * sizeof(double), G.n2,
+                  (G.n1 + 1) * sizeof(double), G.n2, G.n3, cudaMemcpyHostToDevice);
+  if (!rc) rc = copy3d(ctx, B.st[0][6], dp, dy, b2f, G.n1 * sizeof(double), G.n2 + 1,
+                       G.n1 * sizeof(double), G.n2 + 1, G.n3, cudaMemcpyHostToDevice);
+  if (!rc) rc = copy3d(ctx, B.st[0][7], dp, dy, b3f, G.n1 * sizeof(double), G.n2,
+                       G.n1 * sizeof(double), G.n2, G.n3 + 1, cudaMemcpyHostToDevice);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PMHD_OK;
+}
+
+int pmhd_gpu_download_block(pmhd_mesh* m, int gid, double* u, double* w, double* b1f, double* b2f,
+                            double* b3f) {
+  if (!m) return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  const int b = local_index(m, gid);
+  if (b < 0) return fail(ctx, PMHD_ERR_INPUT, "block not local");
+  const KGeom& G = m->G;
+  const size_t dp = size_t(G.sx) * sizeof(double), dy = size_t(G.n2 + 1);
+  const size_t nc = size_t(G.n1) * G.n2 * G.n3;
+  DevBlock& B = m->hblk[b];
+  std::vector<double> f1, f2, f3;
+  double* p1 = b1f;
+  double* p2 = b2f;
+  double* p3 = b3f;
+  if (u) {  // Bcc needs the faces
+    if (!p1) { f1.resize(size_t(G.n3) * G.n2 * (G.n1 + 1)); p1 = f1.data(); }
+    if (!p2) { f2.resize(size_t(G.n3) * (G.n2 + 1) * G.n1); p2 = f2.data(); }
+    if (!p3) { f3.resize(size_t(G.n3 + 1) * G.n2 * G.n1); p3 = f3.data(); }
+  }
+  int rc = PMHD_OK;
+  if (u)
+    for (int v = 0; v < 5 && !rc; ++v)
+      rc = copy3d(ctx, u + v * nc, G.n1 * sizeof(double), G.n2, B.st[0][v], dp, dy,
+                  G.n1 * sizeof(double), G.n2, G.n3, cudaMemcpyDeviceToHost);
+  if (p1 && !rc) rc = copy3d(ctx, p1, (G.n1 + 1) * sizeof(double), G.n2, B.st[0][5], dp, dy,
+                             (G.n1 + 1) * sizeof(double), G.n2, G.n3, cudaMemcpyDeviceToHost);
+  if (p2 && !rc) rc = copy3d(ctx, p2, G.n1 * sizeof(double), G.n2 + 1, B.st[0][6], dp, dy,
+                             G.n1 * sizeof(double), G.n2 + 1, G.n3, cudaMemcpyDeviceToHost);
+  if (p3 && !rc) rc = copy3d(ctx, p3, G.n1 * sizeof(double), G.n2, B.st[0][7], dp, dy,
+                             G.n1 * sizeof(double), G.n2, G.n3 + 1, cudaMemcpyDeviceToHost);
+  if (rc) return rc;
+  if (w) {
+    rc = reset_red(m);
+    if (rc) return rc;
+    launch_c2p_all(m->dblk, G, m->ph, 0, m->dred, 0, ctx->stream);
+    for (int v = 0; v < 8 && !rc; ++v)
+      rc = copy3d(ctx, w + v * nc, G.n1 * sizeof(double), G.n2, B.w[v], dp, dy,
+                  G.n1 * sizeof(double), G.n2, G.n3, cudaMemcpyDeviceToHost);
+    if (rc) return rc;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (u) {  // face_to_center_b, same IEEE ops as the kernels
+    for (int k = 0; k < G.n3; ++k)
+      for (int j = 0; j < G.n2; ++j)
+        for (int i = 0; i < G.n1; ++i) {
+          const size_t c = (size_t(k) * G.n2 + j) * G.n1 + i;
+          const size_t q1 = (size_t(k) * G.n2 + j) * (G.n1 + 1) + i;
+          const size_t q2 = (size_t(k) * (G.n2 + 1) + j) * G.n1 + i;
+          const size_t q3 = (size_t(k) * G.n2 + j) * G.n1 + i;
+          u[5 * nc + c] = 0.5 * (p1[q1] + p1[q1 + 1]);
+          u[6 * nc + c] = 0.5 * (p2[q2] + p2[q2 + G.n1]);
+          u[7 * nc + c] = 0.5 * (p3[q3] + p3[q3 + size_t(G.n2) * G.n1]);
+        }
+  }
+  return PMHD_OK;
+}
+
+int pmhd_gpu_exchange(pmhd_mesh* m) {
+  if (!m) return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  if (!m->all_local) return fail(ctx, PMHD_ERR_INPUT, "exchange needs all neighbours local");
+  launch_exchange(m->dblk, m->G, 0, ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PMHD_OK;
+}
+
+int pmhd_gpu_new_dt(pmhd_mesh* m, double* dt_out, pmhd_status* st) {
+  if (!m || !dt_out) return PMHD_ERR_INPUT;
+  int rc = reset_red(m);
+  if (rc) return rc;
+  launch_dt_from_state(m->dblk, m->G, m->ph, m->dred, m->ctx->stream);
+  return finish(m, 0, 0, dt_out, st);
+}
+
+int pmhd_gpu_stage(pmhd_mesh* m, int stage, double dt, double* dt_next, pmhd_status* st) {
+  if (!m) return PMHD_ERR_INPUT;
+  if (stage != 1 && stage != 2) return fail(m->ctx, PMHD_ERR_INPUT, "stage must be 1 or 2");
+  if (!m->all_local) return fail(m->ctx, PMHD_ERR_INPUT, "stage needs all neighbours local");
+  int rc = reset_red(m);
+  if (!rc) rc = enqueue_stage(m, stage, dt);
+  if (rc) return rc;
+  return finish(m, stage, stage, stage == 2 ? dt_next : nullptr, st);
+}
+
+int pmhd_gpu_vl2_step(pmhd_mesh* m, double dt, double* dt_next, pmhd_status* st) {
+  if (!m) return PMHD_ERR_INPUT;
+  if (!m->all_local) return fail(m->ctx, PMHD_ERR_INPUT, "step needs all neighbours local");
+  int rc = reset_red(m);
+  if (!rc) rc = enqueue_stage(m, 1, dt);
+  if (!rc) rc = enqueue_stage(m, 2, dt);
+  if (rc) return rc;
+  return finish(m, 1, 2, dt_next, st);
+}
+
+int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int* cycles_done,
+                 pmhd_status* st) {
+  if (!m || !t || !dt) return PMHD_ERR_INPUT;
+  int rc = PMHD_OK;
+  if (!(*dt > 0.0)) {
+    rc = pmhd_gpu_new_dt(m, dt, st);
+    if (rc) return rc;
+  }
+  int n = 0;
+  long long floors = 0;
+  while ((ncycles < 0 || n < ncycles) && (!(tlim > 0.0) || *t < tlim)) {
+    double h = *dt;
+    bool last = false;
+    if (tlim > 0.0 && *t + h >= tlim) { h = tlim - *t; last = true; }
+    pmhd_status s;
+    double dn = 0.0;
+    rc = pmhd_gpu_vl2_step(m, h, &dn, &s);
+    floors += s.floor_count;
+    if (rc) { if (st) *st = s; break; }
+    *t = last ? tlim : *t + h;
+    *dt = dn;
+    ++n;
+  }
+  if (cycles_done) *cycles_done = n;
+  if (st && rc == PMHD_OK) { st->code = PMHD_OK; st->floor_count = floors; }
+  return rc;
+}
+
+int pmhd_gpu_diag(pmhd_mesh* m, int kind, double* out) {
+  if (!m || !out) return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  const KGeom& G = m->G;
+  if (kind == PMHD_DIAG_DIVB_MAX) {
+    int rc = reset_red(m);
+    if (rc) return rc;
+    launch_divb(m->dblk, G, m->dred, ctx->stream);
+    rc = fetch_red(m);
+    if (rc) return rc;
+    out[0] = bits2d(m->hred[0].divb_bits);
+    return PMHD_OK;
+  }
+  if (kind == PMHD_DIAG_SUMS) {
+    const int nrow = (G.ke - G.ks) * (G.je - G.js);
+    std::vector<double> rows(size_t(G.nb) * 5 * nrow);
+    launch_row_sums(m->dblk, G, m->drows, ctx->stream);
+    CK(cudaMemcpyAsync(rows.data(), m->drows, rows.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int v = 0; v < 5; ++v) out[v] = 0.0;
+    // blocks in gid order (oracle order); rows in (k, j) order
+    std::vector<int> order(G.nb);
+    for (int b = 0; b < G.nb; ++b) order[b] = b;
+    for (int a = 0; a < G.nb; ++a)
+      for (int c = a + 1; c < G.nb; ++c)
+        if (m->gids[order[c]] < m->gids[order[a]]) std::swap(order[a], order[c]);
+    for (int q = 0; q < G.nb; ++q) {
+      const int b = order[q];
+      for (int v = 0; v < 5; ++v) {
+        double s = 0.0;
+        const double* r = rows.data() + (size_t(b) * 5 + v) * nrow;
+        for (int n = 0; n < nrow; ++n) s += r[n];
+        out[v] += s;
+      }
+    }
+    return PMHD_OK;
+  }
+  return fail(ctx, PMHD_ERR_INPUT, "unknown diagnostic");
+}
+
+int pmhd_gpu_set_profiling(pmhd_mesh* m, int on) {
+  if (!m) return PMHD_ERR_INPUT;
+  m->prof = on != 0;
+  return PMHD_OK;
+}
+
+int pmhd_gpu_region_times(pmhd_mesh* m, pmhd_region_times* out, int reset) {
+  if (!m) return PMHD_ERR_INPUT;
+  if (out) *out = m->times;
+  if (reset) std::memset(&m->times, 0, sizeof(m->times));
+  return PMHD_OK;
+}
+
+}  // extern "C"
+
+extern "C" void* pmhd_gpu_stream(const pmhd_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }

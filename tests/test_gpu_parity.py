@@ -1,0 +1,173 @@
+"""GPU parity tests: the CUDA path (through the C-ABI, include/pmhd_gpu.h)
+against the CPU oracle on the same seeded inputs.
+
+* parity build (libpmhd_gpu_parity.so, --fmad=false): bit-identical fields,
+  dt, floor counts and error locations;
+* product build (libpmhd_gpu.so, FMA): per-cell scaled difference
+  |a-b| <= 1e-11 * max(|b|, max_domain|b_q|) after N cycles (north_star
+  tolerance), identical floor counts.
+"""
+import numpy as np
+import pytest
+
+from paper_1905_04341_b200 import RunConfig, UnphysicalStateError, ConfigError, l1_error
+from paper_1905_04341_b200.solver import GpuSolver
+from oracle.binding import OracleSolver
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+
+CASES = {
+    # name: (config kwargs, cycles)
+    "wave3d_1blk": (dict(nx1=32, nx2=16, nx3=16, mb1=32, mb2=16, mb3=16, x2max=0.5, x3max=0.5,
+                         wave_n1=1, wave_n2=1, wave_amp=1e-3), 5),
+    "wave3d_4blk": (dict(nx1=32, nx2=16, nx3=16, mb1=16, mb2=16, mb3=8, x2max=0.5, x3max=0.5,
+                         wave_n1=1, wave_n3=1, wave_mode=5, wave_amp=1e-3), 4),
+    "ot2d_4blk": (dict(nx1=64, nx2=64, nx3=1, mb1=32, mb2=32, mb3=1, pgen="orszag_tang", cfl=0.4), 20),
+    "blast3d_8blk_floor": (dict(nx1=32, nx2=32, nx3=32, mb1=16, mb2=16, mb3=16, x1min=-0.5, x1max=0.5,
+                                x2min=-0.5, x2max=0.5, x3min=-0.5, x3max=0.5, pgen="blast",
+                                eos_mode="floor", blast_r=0.2), 8),
+    "wave3d_hlle_vl_arith": (dict(nx1=16, nx2=16, nx3=16, mb1=16, mb2=16, mb3=16, wave_n1=1,
+                                  wave_n2=1, wave_n3=1, wave_amp=1e-2, riemann="hlle",
+                                  limiter="vanleer", emf="arith"), 4),
+    "turb3d": (dict(nx1=24, nx2=24, nx3=24, mb1=12, mb2=24, mb3=12, pgen="turbulence"), 4),
+}
+
+
+def run_pair(cfg, ncyc, parity):
+    o = OracleSolver(cfg, workers=8)
+    g = GpuSolver(cfg, parity=parity)
+    o.load_pgen()
+    g.load_pgen()
+    dto, dtg = o.new_dt(), g.new_dt()
+    fo = fg = 0
+    dts = []
+    for _ in range(ncyc):
+        dno, sto = o.vl2_step(dto)
+        dng, stg = g.vl2_step(dto)  # same dt sequence on both sides
+        fo += sto.floor_count
+        fg += stg.floor_count
+        dts.append((dno, dng))
+        dto = dno
+    return o, g, (dto, dtg), (fo, fg), dts
+
+
+def blocks(s, cfg):
+    return [s.get_block(gid) for gid in range(cfg.nblocks)]
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_parity_build_bitwise(gpu_available, name):
+    kw, ncyc = CASES[name]
+    cfg = RunConfig(**kw)
+    o, g, (d0o, d0g), (fo, fg), dts = run_pair(cfg, ncyc, parity=True)
+    assert d0o == d0g
+    for a, b in dts:
+        assert a == b
+    assert fo == fg
+    for gid in range(cfg.nblocks):
+        bo, bg = o.get_block(gid), g.get_block(gid)
+        for f in ("u", "b1f", "b2f", "b3f"):
+            x, y = getattr(bo, f), getattr(bg, f)
+            if not np.array_equal(x, y):
+                bad = np.argwhere(x != y)
+                pytest.fail(f"{name} block {gid} field {f}: {len(bad)} mismatches, first {bad[:3].tolist()}"
+                            f" oracle={x[tuple(bad[0])]!r} gpu={y[tuple(bad[0])]!r}")
+    assert o.divb_max() == g.divb_max()
+    assert np.array_equal(o.sums(), g.sums())
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_fma_build_within_tolerance(gpu_available, name):
+    kw, ncyc = CASES[name]
+    cfg = RunConfig(**kw)
+    o, g, _, (fo, fg), dts = run_pair(cfg, ncyc, parity=False)
+    assert fo == fg
+    for a, b in dts:
+        assert abs(a - b) <= 1e-12 * a
+    ks, js, is_ = cfg.active_slices()
+    worst = 0.0
+    for gid in range(cfg.nblocks):
+        bo, bg = o.get_block(gid), g.get_block(gid)
+        for q in range(8):
+            x = bo.u[q, ks, js, is_]
+            y = bg.u[q, ks, js, is_]
+            sq = np.max(np.abs(x)) if np.max(np.abs(x)) > 0 else 1.0
+            worst = max(worst, float(np.max(np.abs(x - y) / np.maximum(np.abs(x), sq))))
+    assert worst <= TOL, worst
+    assert g.divb_max() <= max(1e-11, 10 * o.divb_max())
+
+
+def test_linear_wave_l1_and_order_on_gpu(gpu_available):
+    """Identical L1 error and convergence order as the oracle (north_star)."""
+    errs_o, errs_g = [], []
+    for n in (32, 64):
+        cfg = RunConfig(nx1=n, nx2=8, nx3=8, mb1=n, mb2=8, mb3=8, x2max=8.0 / n, x3max=8.0 / n)
+        tl = cfg.default_tlim()
+        o = OracleSolver(cfg, workers=8)
+        o.load_pgen()
+        to, *_ = o.run(tlim=tl)
+        g = GpuSolver(cfg, parity=False)
+        g.load_pgen()
+        tg, *_ = g.run(tlim=tl)
+        assert to == tg
+        errs_o.append(l1_error(cfg, blocks(o, cfg), to)[1])
+        errs_g.append(l1_error(cfg, blocks(g, cfg), tg)[1])
+    for a, b in zip(errs_o, errs_g):
+        assert abs(a - b) <= 1e-9 * a
+    order = np.log2(errs_g[0] / errs_g[1])
+    assert order >= 1.9
+
+
+def test_upload_download_roundtrip(gpu_available):
+    cfg = RunConfig(nx1=16, nx2=12, nx3=8, mb1=8, mb2=12, mb3=8, pgen="turbulence")
+    g = GpuSolver(cfg)
+    rng = np.random.default_rng(0)
+    for gid in range(cfg.nblocks):
+        b = cfg.new_block()
+        for f in ("u", "b1f", "b2f", "b3f"):
+            getattr(b, f)[:] = rng.normal(size=getattr(b, f).shape)
+        g.set_block(gid, b)
+        r = g.get_block(gid)
+        for f in ("b1f", "b2f", "b3f"):
+            assert np.array_equal(getattr(b, f), getattr(r, f))
+        assert np.array_equal(b.u[:5], r.u[:5])
+        bcc1 = 0.5 * (b.b1f[:, :, :-1] + b.b1f[:, :, 1:])
+        assert np.array_equal(r.u[5], bcc1)
+
+
+def test_config_errors(gpu_available):
+    with pytest.raises(ConfigError):
+        GpuSolver(RunConfig(nx1=48, nx2=32, nx3=32, mb1=32, mb2=32, mb3=32))
+    with pytest.raises(ConfigError):
+        GpuSolver(RunConfig(nx1=16, nx2=16, nx3=16, mb1=16, mb2=16, mb3=16, ng=1))
+
+
+def test_unphysical_error_matches_oracle(gpu_available):
+    cfg = RunConfig(nx1=8, nx2=8, nx3=8, mb1=8, mb2=8, mb3=8, pgen="uniform", rho=1, p=1e-3,
+                    b1=0.0, b2=0.0, b3=0.0)
+    b = cfg.pgen_block(0)
+    b.u[4, 2 + 3, 2 + 1, 2 + 6] = -1.0
+    b.u[4, 2 + 5, 2 + 0, 2 + 2] = -1.0
+    errs = []
+    for s in (OracleSolver(cfg), GpuSolver(cfg, parity=True), GpuSolver(cfg)):
+        s.set_block(0, b)
+        s.exchange()
+        with pytest.raises(UnphysicalStateError) as ei:
+            s.vl2_step(1e-3)
+        errs.append((ei.value.stage_tag, ei.value.kk, ei.value.jj, ei.value.ii))
+    assert errs[0] == ("stage1", 3, 1, 6)
+    assert errs[0] == errs[1] == errs[2]
+
+
+def test_run_loop_lands_on_tlim(gpu_available):
+    cfg = RunConfig(nx1=16, nx2=16, nx3=16, mb1=16, mb2=16, mb3=16)
+    tl = 0.05
+    o = OracleSolver(cfg)
+    o.load_pgen()
+    to, no, *_ = o.run(tlim=tl)
+    g = GpuSolver(cfg, parity=True)
+    g.load_pgen()
+    tg, ng_, *_ = g.run(tlim=tl)
+    assert to == tg == tl and no == ng_
+    assert np.array_equal(o.get_block(0).u, g.get_block(0).u)
