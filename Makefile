@@ -13,7 +13,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -Xlinker -Bsymbolic -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Iinclude -I$(GPUSRC) \
             -Xptxas -warn-spills --expt-relaxed-constexpr
 HOSTFLAGS:= -std=c++20 -O2 -march=x86-64-v3 -fPIC -Wall -Wextra -Iinclude
-GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu
+GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu $(GPUSRC)/kernels_flux.cu
 GPU_DEPS := $(GPU_SRCS) $(wildcard $(GPUSRC)/*.cuh) include/pmhd_gpu.h
 
 all: host gpu oracle
@@ -41,3 +41,9 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all host gpu oracle clean
+
+# A/B experiment builds (bench.py honours PMHD_GPU_LIB=<path>)
+exp: $(GPU_DEPS)
+	@mkdir -p $(LIB)/exp
+	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_MINB=5 -shared -o $(LIB)/exp/libpmhd_gpu_minb5.so $(GPU_SRCS)
+	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_MINB=3 -shared -o $(LIB)/exp/libpmhd_gpu_minb3.so $(GPU_SRCS)

@@ -421,17 +421,23 @@ inline R plm_slope(R qm, R q0, R qp, int limiter) {
 // Riemann solve at one face + the CT by-products.  out: 5 hydro fluxes in the
 // ROTATED order (d, mn, mt1, mt2, e), ey = -F(bt1), ez = F(bt2) (the face
 // electric fields, E = -v x B, Athena++ convention), and the
-// contact-upwind weight (1: upwind cell is the low side, 0: high side,
-// 1/2: zero mass flux; Gardiner & Stone 2005 Eq. 50).
+// contact-upwind weight (1: upwind cell is the low side, 0: high side;
+// Gardiner & Stone 2005 Eq. 50).  The weight is the continuous Athena++ form
+// w = 1/2 + clamp(1024 (dt/dx) F_rho / (rho_L + rho_R), -1/2, 1/2) [ext]:
+// a pure sign(F_rho) switch flips 0 <-> 1 on round-off noise of a vanishing
+// mass flux and turns 1-ulp differences into O(dt dE) field differences.
+// c1024 = 1024 * dt / dx_dir (full-cycle dt, both stages).
 template <class R>
-inline void face_solve(const R* wl, const R* wr, R bx, const Phys& ph, R* out) {
+inline void face_solve(const R* wl, const R* wr, R bx, const Phys& ph, double c1024, R* out) {
+  using std::fmin; using std::fmax;
   R flx[7];
   if (ph.riemann == PMHD_RIEMANN_HLLE) riemann_hlle(wl, wr, bx, ph, flx);
   else riemann_hlld(wl, wr, bx, ph, flx);
   for (int n = 0; n < 5; ++n) out[n] = flx[n];
   out[5] = -flx[5];
   out[6] = flx[6];
-  out[7] = (flx[0] > 0.0) ? R(1.0) : ((flx[0] < 0.0) ? R(0.0) : R(0.5));
+  const R vc = c1024 * flx[0] / (wl[0] + wr[0]);
+  out[7] = 0.5 + fmax(R(-0.5), fmin(R(0.5), vc));
 }
 
 //============================================================================
@@ -570,9 +576,10 @@ class Mesh {
   // Riemann fluxes in direction dir over the face range needed by CT
   // (SURVEY.md Appendix A.2): normal faces [s, e], transverse extended by one
   // cell on each side (by one layer in x3 only in 3D).
-  void fluxes(Block<R>& B, const State<R>& in, int dir, bool plm) {
+  void fluxes(Block<R>& B, const State<R>& in, int dir, bool plm, double dt) {
     int iv[3], ib[2];
     rot_indices(dir, iv, ib);
+    const double c1024 = 1024.0 * dt / g.dx[dir];
     const int d3 = (g.dim == 3) ? 1 : 0;
     Bounds fb;
     if (dir == 0) fb = Bounds{g.ks - d3, g.ke + d3, g.js - 1, g.je + 1, g.is, g.ie + 1};
@@ -598,7 +605,7 @@ class Mesh {
         }
       }
       R out[8];
-      face_solve(wl, wr, bn(k, j, i), ph, out);
+      face_solve(wl, wr, bn(k, j, i), ph, c1024, out);
       B.fx[dir][IDN](k, j, i) = out[0];  // un-rotate momentum fluxes
       B.fx[dir][iv[0]](k, j, i) = out[1];
       B.fx[dir][iv[1]](k, j, i) = out[2];
@@ -813,7 +820,7 @@ class Mesh {
     for (auto& B : blocks) {
       const State<R>& in = (s == 1) ? B.A : B.B;
       c2p_all(B, in, bad);
-      for (int dir = 0; dir < g.dim; ++dir) fluxes(B, in, dir, s == 2);
+      for (int dir = 0; dir < g.dim; ++dir) fluxes(B, in, dir, s == 2, dt);
       emfs(B);
       State<R>& out = (s == 1) ? B.B : B.A;
       update(B, B.A, out, (s == 1) ? 0.5 : 1.0, dt, bad, nfloor);

@@ -48,6 +48,7 @@ struct DevRed {
 // IEEE operations as the oracle.
 struct KStage {
   double c1, c2, c3;
+  double c1024[3];  // 1024 * dt / dx_d (contact-upwind weight scale)
   int in_sel, out_sel, stage, plm;
 };
 
@@ -55,7 +56,9 @@ struct KStage {
 void launch_c2p_all(const DevBlock* blks, const KGeom& G, const KPhys& ph, int sel, DevRed* red,
                     int stage, cudaStream_t s);
 void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel, int plm,
-                 cudaStream_t s);
+                 double c1024, cudaStream_t s);
+void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
+                       int plm, double c1024, int stage, DevRed* red, cudaStream_t s);
 void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s);
 void launch_update(const DevBlock* blks, const KGeom& G, const KStage& ks, cudaStream_t s);
 void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,

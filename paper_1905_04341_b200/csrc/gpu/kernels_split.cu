@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(TX* TY) k_c2p_all(const DevBlock* __restrict__
 
 template <int DIR>
 __global__ void __launch_bounds__(TX* TY) k_flux(const DevBlock* __restrict__ blks, KGeom G, KPhys ph,
-                                                 int sel, int plm, Box bx) {
+                                                 int sel, int plm, double c1024, Box bx) {
   BOX_INDEX(bx);
   const DevBlock& B = blks[b];
   const long long off = (DIR == 0) ? 1 : ((DIR == 1) ? G.sx : G.sy);
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(TX* TY) k_flux(const DevBlock* __restrict__ bl
     }
   }
   double out[8];
-  face_solve(wl, wr, B.st[sel][5 + DIR][id], ph, out);
+  face_solve(wl, wr, B.st[sel][5 + DIR][id], ph, c1024, out);
   double* const* F = B.fx[DIR];
   F[0][id] = out[0];
   F[V1][id] = out[1];
@@ -362,16 +362,16 @@ void launch_c2p_all(const DevBlock* blks, const KGeom& G, const KPhys& ph, int s
 }
 
 void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel, int plm,
-                 cudaStream_t s) {
+                 double c1024, cudaStream_t s) {
   const int d3 = (G.dim == 3) ? 1 : 0;
   Box bx;
   if (dir == 0) bx = Box{G.ks - d3, G.ke + d3, G.js - 1, G.je + 1, G.is, G.ie + 1};
   else if (dir == 1) bx = Box{G.ks - d3, G.ke + d3, G.js, G.je + 1, G.is - 1, G.ie + 1};
   else bx = Box{G.ks, G.ke + 1, G.js - 1, G.je + 1, G.is - 1, G.ie + 1};
   const dim3 g = grid_for(bx, G.nb);
-  if (dir == 0) k_flux<0><<<g, tb(), 0, s>>>(blks, G, ph, sel, plm, bx);
-  else if (dir == 1) k_flux<1><<<g, tb(), 0, s>>>(blks, G, ph, sel, plm, bx);
-  else k_flux<2><<<g, tb(), 0, s>>>(blks, G, ph, sel, plm, bx);
+  if (dir == 0) k_flux<0><<<g, tb(), 0, s>>>(blks, G, ph, sel, plm, c1024, bx);
+  else if (dir == 1) k_flux<1><<<g, tb(), 0, s>>>(blks, G, ph, sel, plm, c1024, bx);
+  else k_flux<2><<<g, tb(), 0, s>>>(blks, G, ph, sel, plm, c1024, bx);
 }
 
 void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s) {

@@ -10,6 +10,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -49,6 +50,7 @@ struct pmhd_mesh {
   double* drows = nullptr;
   bool all_local = true;
   bool prof = false;
+  int variant = 0;                // 0: fused flux kernels; 1: split (debug; PMHD_KERNELS=split)
   cudaEvent_t ev[8] = {};
   pmhd_region_times times{};
 };
@@ -134,6 +136,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt) {
   ks.c1 = bdt / G.dx[0];
   ks.c2 = bdt / G.dx[1];
   ks.c3 = bdt / G.dx[2];
+  for (int d = 0; d < 3; ++d) ks.c1024[d] = 1024.0 * dt / G.dx[d];
   ks.in_sel = (s == 1) ? 0 : 1;
   ks.out_sel = (s == 1) ? 1 : 0;
   ks.stage = s;
@@ -142,7 +145,12 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt) {
   rec(m, 0);
   launch_c2p_all(m->dblk, G, m->ph, ks.in_sel, m->dred, s, st);
   rec(m, 1);
-  for (int dir = 0; dir < G.dim; ++dir) launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, st);
+  for (int dir = 0; dir < G.dim; ++dir) {
+    if (m->variant == 0)
+      launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], s, m->dred, st);
+    else
+      launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], st);
+  }
   rec(m, 2);
   launch_emf(m->dblk, G, m->ph, st);
   rec(m, 3);
@@ -287,6 +295,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
     }
   }
   G.nb = int(m->gids.size());
+  if (const char* kv = std::getenv("PMHD_KERNELS")) m->variant = (std::string(kv) == "split") ? 1 : 0;
   m->ph.gamma = desc->gamma;
   m->ph.gm1 = desc->gamma - 1.0;
   m->ph.igm1 = 1.0 / (desc->gamma - 1.0);

@@ -152,6 +152,10 @@ GPU_SYMBOLS = [
 
 
 def gpu_lib_path(parity: bool = False) -> Path:
+    # PMHD_GPU_LIB: A/B experiments with an alternative in-tree build of the
+    # same sources (e.g. lib/exp/*.so); never a CPU substitute.
+    if not parity and os.environ.get("PMHD_GPU_LIB"):
+        return Path(os.environ["PMHD_GPU_LIB"]).resolve()
     return LIB_DIR / ("libpmhd_gpu_parity.so" if parity else "libpmhd_gpu.so")
 
 

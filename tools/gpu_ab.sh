@@ -1,0 +1,24 @@
+#!/bin/bash
+# A/B bench session: parity tests, then short benches of variants.
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -4 gpurun_out/pytest_gpu.log
+B="python bench.py --steps 6 --warmup 3 --no-cpu-baseline --no-e2e"
+for v in "$@"; do
+  case $v in
+    split) PMHD_KERNELS=split $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    default) $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    parity) PMHD_GPU_LIB=paper_1905_04341_b200/lib/libpmhd_gpu_parity.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    *) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_$v.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+  esac
+  python - "$v" <<'PY'
+import json,sys
+v=sys.argv[1]
+try:
+    d=json.load(open(f"gpurun_out/ab_{v}.json"))
+    r=d["roofline"]
+    print(f"{v:10s} cups={d['value']:.4g} ms/step={d['ms_per_step']:.3f} fp64frac={r['fp64']['frac']:.3f} shares={ {k:round(x,3) for k,x in r['region_share'].items()} } clk={d['clocks']}")
+except Exception as e:
+    print(v, "FAILED", e, open(f"gpurun_out/ab_{v}.err").read()[-500:])
+PY
+done
