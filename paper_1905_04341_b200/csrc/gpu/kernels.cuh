@@ -28,10 +28,16 @@ struct KGeom {
 };
 
 struct DevBlock {
-  double* st[2][kNState];  // state A (0) and B (1)
+  // st[0] = u^n (current), st[1] = u^{n+1/2}, st[2] = u^{n+1} (next).  The
+  // ABI keeps two device copies of the block table with st[0] and st[2]
+  // swapped and flips between them after each cycle, so no stage updates a
+  // buffer that another tile still reads (tiles recompute shared faces).
+  double* st[3][kNState];
   double* w[8];            // stage-input primitives incl. Bcc (split kernels)
   double* fx[3][8];        // face data: 5 lab-order fluxes, ey, ez, weight
-  double* e[3];            // corner EMFs e1, e2, e3
+  double* e[3];            // corner EMFs e1, e2, e3 (split kernels)
+  double* ec[3];           // cell-centred E = -v x B of the stage input (fused
+                           // kernels; aliases e[], which they do not use)
   int c[3];                // block coordinates
   int nbr[3][2];           // local index of the lower / upper neighbour
 };
@@ -49,7 +55,7 @@ struct DevRed {
 struct KStage {
   double c1, c2, c3;
   double c1024[3];  // 1024 * dt / dx_d (contact-upwind weight scale)
-  int in_sel, out_sel, stage, plm;
+  int in_sel, out_sel, stage, plm;  // base is always st[0]
 };
 
 // Launchers (kernels.cu).
@@ -60,6 +66,8 @@ void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir,
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
                        int plm, double c1024, int stage, DevRed* red, cudaStream_t s);
 void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s);
+void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
+                         DevRed* red, int want_dt, cudaStream_t s);
 void launch_update(const DevBlock* blks, const KGeom& G, const KStage& ks, cudaStream_t s);
 void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                     DevRed* red, int want_dt, cudaStream_t s);

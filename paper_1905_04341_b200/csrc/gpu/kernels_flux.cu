@@ -7,12 +7,17 @@
 //
 // Tiling: a CTA of 128 threads owns 32 x 8 faces: 32 consecutive faces along
 // i (coalesced HBM rows) times 8 positions along the second tile axis (j for
-// x1/x2 faces, k for x3 faces) in one plane (x1/x2) or one row (x3).  The
-// stencil cells of the tile (36 x 8 for x1, 32 x 11 for x2/x3) are loaded once
-// with coalesced loads, converted to primitives (7 rotated variables) and kept
-// in shared memory; each thread then solves 2 faces reading its stencil from
-// shared memory, so no warp waits on HBM during the Riemann solve.  Several
-// CTAs per SM overlap one tile's load phase with other tiles' solves.
+// x1/x2 faces, k for x3 faces) in one plane (x1/x2) or one row (x3).
+//  phase 1  the stencil cells of the tile (36 x 8 for x1, 32 x 11 for x2/x3)
+//           are loaded once with coalesced loads and converted to the 7
+//           rotated primitives in shared memory;
+//  phase 2  each cell's PLM slope is formed ONCE per variable and the two
+//           reconstructed interface values q -/+ dq/2 replace it in shared
+//           memory (stage 2 only; stage 1 is donor cell);
+//  phase 3  each thread solves 2 faces from shared memory (no HBM waits).
+// The last direction's kernel also writes the cell-centred E = -v x B of the
+// box the fused update kernel needs (cells [is-1,ie] x [js-1,je] x [ks-1,ke]),
+// so that kernel does not redo cons_to_prim.
 #include "kernels.cuh"
 
 namespace pmhd_gpu {
@@ -31,6 +36,8 @@ struct TileShape {
   static constexpr int NCOL = (DIR == 0) ? FX + 4 : FX;  // cells along i
   static constexpr int NROW = (DIR == 0) ? FS : FS + 3;  // cells along the 2nd axis
   static constexpr int NCELL = NCOL * NROW;
+  static constexpr int DC = (DIR == 0) ? 1 : NCOL;       // stencil stride in the tile
+  static constexpr int PER = (NCELL + NTHR - 1) / NTHR;  // cells per thread
 };
 
 // Lab index of the 7 rotated variables (d, vn, vt1, vt2, p, bt1, bt2).
@@ -42,10 +49,12 @@ __device__ __forceinline__ int rot_var(int n) {
 
 template <int DIR>
 __global__ void __launch_bounds__(NTHR, PMHD_FLUX_MINB)
-k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024, int stage,
-             DevRed* red, int f_i0, int f_i1, int f_s0, int f_s1, int f_t0, int f_t1) {
+k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024,
+             int stage, DevRed* red, int write_ec, int f_i0, int f_i1, int f_s0, int f_s1, int f_t0,
+             int f_t1) {
   using TS = TileShape<DIR>;
-  __shared__ double sw[7][TS::NCELL];
+  __shared__ double sw[7][TS::NCELL];  // primitives; after phase 2: q - dq/2 (low-face value)
+  __shared__ double sp[7][TS::NCELL];  // after phase 2: q + dq/2 (high-face value)
 
   const int nt = f_t1 - f_t0;
   const int b = blockIdx.z / nt;
@@ -77,34 +86,69 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       const long long gk = (G.dim == 3) ? (long long)B.c[2] * G.mb[2] + (k - G.ks) : 0;
       atomicMin(&red[stage].bad_key, (unsigned long long)((gk * G.nx[1] + gj) * G.nx[0] + gi));
     }
+    if (DIR != 0 && write_ec) {
+      // cells of this tile's own face rows [fs0, fs0+8) clipped to the face
+      // range, plus the row below the block's first face row
+      const int s = (DIR == 2) ? k : j;
+      const bool own = (s >= fs0 && s < fs0 + FS && s < f_s1) || (fs0 == f_s0 && s == f_s0 - 1);
+      if (own && i >= f_i0 && i < f_i1) {
+        B.ec[0][id] = w[3] * w[6] - w[2] * w[7];
+        B.ec[1][id] = w[1] * w[7] - w[3] * w[5];
+        B.ec[2][id] = w[2] * w[5] - w[1] * w[6];
+      }
+    }
 #pragma unroll
     for (int n = 0; n < 7; ++n) sw[n][c] = w[rot_var<DIR>(n)];
   }
   __syncthreads();
 
-  // ---- phase 2: two faces per thread ---------------------------------------
+  // ---- phase 2: per-cell reconstruction, one variable at a time ------------
+  if (plm) {
+    constexpr int LEN = (DIR == 0) ? TS::NCOL : TS::NROW;
+#pragma unroll 1
+    for (int n = 0; n < 7; ++n) {
+      double lo[TS::PER], hi[TS::PER];
+#pragma unroll
+      for (int p = 0; p < TS::PER; ++p) {
+        const int c = threadIdx.x + p * NTHR;
+        const int pos = (DIR == 0) ? c % TS::NCOL : c / TS::NCOL;
+        lo[p] = hi[p] = 0.0;
+        if (c < TS::NCELL && pos >= 1 && pos <= LEN - 2) {
+          const double q0 = sw[n][c];
+          const double dq = plm_slope(sw[n][c - TS::DC], q0, sw[n][c + TS::DC], ph.limiter);
+          hi[p] = q0 + 0.5 * dq;  // wL of the face above (oracle: qm1 + 0.5*slope)
+          lo[p] = q0 - 0.5 * dq;  // wR of the face below (oracle: q0 - 0.5*slope)
+        }
+      }
+      __syncthreads();  // all reads of sw[n] done before it is overwritten
+#pragma unroll
+      for (int p = 0; p < TS::PER; ++p) {
+        const int c = threadIdx.x + p * NTHR;
+        const int pos = (DIR == 0) ? c % TS::NCOL : c / TS::NCOL;
+        if (c < TS::NCELL && pos >= 1 && pos <= LEN - 2) {
+          sw[n][c] = lo[p];
+          sp[n][c] = hi[p];
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- phase 3: two faces per thread ---------------------------------------
   const int fc = threadIdx.x % FX;
+  const double* const wsrc = plm ? &sp[0][0] : &sw[0][0];  // low-side cell's high-face value
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
     const int fr = threadIdx.x / FX + 4 * h;
     const int fi = fi0 + fc, fs = fs0 + fr;
     if (fi >= f_i1 || fs >= f_s1) continue;
-    // stencil cell index of (cell on the low side - 1) ... (high side + 1)
-    int c0, dc;
-    if (DIR == 0) { c0 = fr * TS::NCOL + fc; dc = 1; }
-    else { c0 = fr * TS::NCOL + fc; dc = TS::NCOL; }
+    const int cl = fr * TS::NCOL + fc + TS::DC;  // cell on the low side of the face
+    const int ch = cl + TS::DC;                  // cell on the high side
     double wl[7], wr[7];
 #pragma unroll
     for (int n = 0; n < 7; ++n) {
-      const double qm2 = sw[n][c0], qm1 = sw[n][c0 + dc];
-      const double q0 = sw[n][c0 + 2 * dc], qp1 = sw[n][c0 + 3 * dc];
-      if (plm) {
-        wl[n] = qm1 + 0.5 * plm_slope(qm2, qm1, q0, ph.limiter);
-        wr[n] = q0 - 0.5 * plm_slope(qm1, q0, qp1, ph.limiter);
-      } else {
-        wl[n] = qm1;
-        wr[n] = q0;
-      }
+      wl[n] = wsrc[n * TS::NCELL + cl];
+      wr[n] = sw[n][ch];
     }
     int i, j, k;
     if (DIR == 0) { i = fi; j = fs; k = t3; }
@@ -137,13 +181,17 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   else { k0 = G.ks; k1 = G.ke + 1; j0 = G.js - 1; j1 = G.je + 1; i0 = G.is - 1; i1 = G.ie + 1; }
   const int ns0 = (dir == 2) ? k0 : j0, ns1 = (dir == 2) ? k1 : j1;
   const int nt0 = (dir == 2) ? j0 : k0, nt1 = (dir == 2) ? j1 : k1;
+  const int write_ec = (dir == G.dim - 1) ? 1 : 0;
   const dim3 grid((i1 - i0 + FX - 1) / FX, (ns1 - ns0 + FS - 1) / FS, (nt1 - nt0) * G.nb);
   if (dir == 0)
-    k_flux_fused<0><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, i0, i1, ns0, ns1, nt0, nt1);
+    k_flux_fused<0><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, i1,
+                                          ns0, ns1, nt0, nt1);
   else if (dir == 1)
-    k_flux_fused<1><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, i0, i1, ns0, ns1, nt0, nt1);
+    k_flux_fused<1><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, i1,
+                                          ns0, ns1, nt0, nt1);
   else
-    k_flux_fused<2><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, i0, i1, ns0, ns1, nt0, nt1);
+    k_flux_fused<2><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, i1,
+                                          ns0, ns1, nt0, nt1);
 }
 
 }  // namespace pmhd_gpu

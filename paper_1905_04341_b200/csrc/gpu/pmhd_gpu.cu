@@ -41,8 +41,9 @@ struct pmhd_mesh {
   KGeom G;
   KPhys ph;
   std::vector<int> gids;          // global id of each local block
-  std::vector<DevBlock> hblk;
+  std::vector<DevBlock> hblk, hblk_alt;   // current table and its st[0]<->st[2] swap
   DevBlock* dblk = nullptr;
+  DevBlock* dblk_alt = nullptr;
   double* slab = nullptr;
   size_t arr_elems = 0;
   DevRed* dred = nullptr;         // 3 slots
@@ -138,12 +139,12 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt) {
   ks.c3 = bdt / G.dx[2];
   for (int d = 0; d < 3; ++d) ks.c1024[d] = 1024.0 * dt / G.dx[d];
   ks.in_sel = (s == 1) ? 0 : 1;
-  ks.out_sel = (s == 1) ? 1 : 0;
+  ks.out_sel = (s == 1) ? 1 : 2;
   ks.stage = s;
   ks.plm = (s == 2);
   cudaStream_t st = ctx->stream;
   rec(m, 0);
-  launch_c2p_all(m->dblk, G, m->ph, ks.in_sel, m->dred, s, st);
+  if (m->variant == 1) launch_c2p_all(m->dblk, G, m->ph, ks.in_sel, m->dred, s, st);
   rec(m, 1);
   for (int dir = 0; dir < G.dim; ++dir) {
     if (m->variant == 0)
@@ -152,15 +153,23 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt) {
       launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], st);
   }
   rec(m, 2);
-  launch_emf(m->dblk, G, m->ph, st);
+  if (m->variant == 1) launch_emf(m->dblk, G, m->ph, st);
   rec(m, 3);
-  launch_update(m->dblk, G, ks, st);
-  launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
+  if (m->variant == 0) {
+    launch_update_fused(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
+  } else {
+    launch_update(m->dblk, G, ks, st);
+    launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
+  }
   rec(m, 4);
   launch_exchange(m->dblk, G, ks.out_sel, st);
   rec(m, 5);
-  m->times.kernel_launches += 4 + 2 * G.dim;
+  m->times.kernel_launches += (m->variant == 0) ? 1 + 2 * G.dim : 4 + 2 * G.dim;
   CK(cudaGetLastError());
+  if (s == 2) {  // u^{n+1} (st[2]) becomes the current state: flip the tables
+    std::swap(m->hblk, m->hblk_alt);
+    std::swap(m->dblk, m->dblk_alt);
+  }
   if (m->prof) {
     CK(cudaEventSynchronize(m->ev[5]));
     float t[5];
@@ -306,10 +315,10 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   m->ph.eos = desc->eos_mode;
   m->ph.emf = desc->emf_mode;
 
-  // one slab: 51 arrays per block, each (n3+1)*sy doubles plus a 64-double guard
+  // one slab: 59 arrays per block, each (n3+1)*sy doubles plus a 64-double guard
   const size_t arr = size_t(G.n3 + 1) * size_t(G.sy) + 64;
   m->arr_elems = arr;
-  const size_t per_block = 51 * arr;
+  const size_t per_block = 59 * arr;
   const size_t bytes = per_block * G.nb * sizeof(double);
   if (cudaMalloc(&m->slab, bytes) != cudaSuccess) {
     delete m;
@@ -321,12 +330,13 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
     double* p = m->slab + size_t(b) * per_block + 32;
     DevBlock& B = m->hblk[b];
     auto take = [&]() { double* q = p; p += arr; return q; };
-    for (int s = 0; s < 2; ++s)
+    for (int s = 0; s < 3; ++s)
       for (int v = 0; v < kNState; ++v) B.st[s][v] = take();
     for (int v = 0; v < 8; ++v) B.w[v] = take();
     for (int d = 0; d < 3; ++d)
       for (int v = 0; v < 8; ++v) B.fx[d][v] = take();
     for (int c = 0; c < 3; ++c) B.e[c] = take();
+    for (int c = 0; c < 3; ++c) B.ec[c] = B.e[c];
     const int gid = m->gids[b];
     B.c[0] = gid % nb[0];
     B.c[1] = (gid / nb[0]) % nb[1];
@@ -342,8 +352,15 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
         B.nbr[d][side] = li;
       }
   }
+  // second table with st[0] <-> st[2] swapped (flipped after every cycle)
+  m->hblk_alt = m->hblk;
+  for (auto& B : m->hblk_alt)
+    for (int v = 0; v < kNState; ++v) std::swap(B.st[0][v], B.st[2][v]);
   CK(cudaMalloc(&m->dblk, sizeof(DevBlock) * G.nb));
+  CK(cudaMalloc(&m->dblk_alt, sizeof(DevBlock) * G.nb));
   CK(cudaMemcpyAsync(m->dblk, m->hblk.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(m->dblk_alt, m->hblk_alt.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice,
+                     ctx->stream));
   CK(cudaMalloc(&m->dred, 3 * sizeof(DevRed)));
   CK(cudaMallocHost(&m->hred, 3 * sizeof(DevRed)));
   const size_t nrows = size_t(G.nb) * 5 * (G.ke - G.ks) * (G.je - G.js);
@@ -360,6 +377,7 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   cudaStreamSynchronize(m->ctx->stream);
   cudaFree(m->slab);
   cudaFree(m->dblk);
+  cudaFree(m->dblk_alt);
   cudaFree(m->dred);
   cudaFree(m->drows);
   cudaFreeHost(m->hred);

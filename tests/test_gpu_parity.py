@@ -191,3 +191,15 @@ def test_run_loop_lands_on_tlim(gpu_available):
     tg, ng_, *_ = g.run(tlim=tl)
     assert to == tg == tl and no == ng_
     assert np.array_equal(o.get_block(0).u, g.get_block(0).u)
+
+
+@pytest.mark.parametrize("variant", ["split", "fused"])
+def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
+    """Both kernel organisations (one kernel per reference op, and the fused
+    flux / fused update kernels) are bit-identical to the oracle."""
+    monkeypatch.setenv("PMHD_KERNELS", variant)
+    kw, ncyc = CASES["wave3d_4blk"]
+    cfg = RunConfig(**kw)
+    o, g, _, _, _ = run_pair(cfg, 3, parity=True)
+    for gid in range(cfg.nblocks):
+        assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
