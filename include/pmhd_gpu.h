@@ -160,6 +160,24 @@ int pmhd_gpu_vl2_step(pmhd_mesh* mesh, double dt, double* dt_next, pmhd_status* 
 int pmhd_gpu_run(pmhd_mesh* mesh, int ncycles, double tlim, double* t, double* dt,
                  int* cycles_done, pmhd_status* st);
 
+/* ---- Multi-rank pieces (one process per GPU) -------------
+ * A rank owns a subset of the blocks (gids at mesh creation).  A stage is then
+ * pmhd_gpu_stage_compute + for dir in x1..x3 { pmhd_gpu_exchange_dir (blocks
+ * with local neighbours) + halo pack -> transport -> unpack for the faces with
+ * remote neighbours }, which reproduces exchange_ghosts' sequential sweeps
+ * exactly.  half = 1 selects u^{n+1/2} (after stage 1), 0 the
+ * current state (after stage 2).  Halo buffers are DEVICE pointers; message
+ * layout = pack_boundary: variable-major (u0..u4, b1f, b2f,
+ * b3f), each slab in k-j-i order.  pack/unpack return after the copy is done. */
+int pmhd_gpu_stage_compute(pmhd_mesh* mesh, int stage, double dt, double* dt_next, pmhd_status* st);
+int pmhd_gpu_exchange_dir(pmhd_mesh* mesh, int dir, int half);
+/* doubles in the message that block side `side` (0 lower, 1 upper) receives */
+int pmhd_gpu_halo_count(const pmhd_mesh* mesh, int dir, int side, long long* n);
+/* slab block gid sends to its neighbour on `side` */
+int pmhd_gpu_halo_pack(pmhd_mesh* mesh, int gid, int dir, int side, int half, double* dev_buf);
+/* ghosts of block gid on `side`, from the neighbour's pack(..., 1 - side) */
+int pmhd_gpu_halo_unpack(pmhd_mesh* mesh, int gid, int dir, int side, int half, const double* dev_buf);
+
 /* Diagnostics (PMHD_DIAG_*). */
 int pmhd_gpu_diag(pmhd_mesh* mesh, int kind, double* out);
 

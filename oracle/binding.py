@@ -28,6 +28,14 @@ def lib(ref: bool = False) -> C.CDLL:
         L = C.CDLL(str(path))
         L.oracle_last_error.restype = C.c_char_p
         L.oracle_mesh_create.argtypes = [C.POINTER(N.MeshDesc), C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.oracle_mesh_create_local.argtypes = [C.POINTER(N.MeshDesc), C.c_int, C.c_int,
+                                               C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
+        L.oracle_stage_compute.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, C.POINTER(N.Status)]
+        L.oracle_exchange_dir.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.oracle_halo_count.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.oracle_halo_count.restype = C.c_longlong
+        L.oracle_halo_pack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        L.oracle_halo_unpack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         L.oracle_mesh_destroy.argtypes = [C.c_void_p]
         L.oracle_mesh_destroy.restype = None
         L.oracle_set_workers.argtypes = [C.c_int]
@@ -121,14 +129,43 @@ def flops_reset():
 class OracleSolver:
     """CPU restatement of the reference solver."""
 
-    def __init__(self, cfg, workers: int = 1, counting: bool = False, ref: bool = False):
+    def __init__(self, cfg, workers: int = 1, counting: bool = False, ref: bool = False, gids=None):
         self.cfg = cfg
         self.L = lib(ref)
         self.h = C.c_void_p()
-        rc = self.L.oracle_mesh_create(C.byref(cfg.desc), int(counting), int(workers), C.byref(self.h))
+        if gids is None:
+            rc = self.L.oracle_mesh_create(C.byref(cfg.desc), int(counting), int(workers), C.byref(self.h))
+        else:
+            arr = (C.c_int * len(gids))(*gids)
+            rc = self.L.oracle_mesh_create_local(C.byref(cfg.desc), int(counting), int(workers), arr,
+                                                 len(gids), C.byref(self.h))
         if rc != N.PMHD_OK:
             raise ConfigError(self.L.oracle_last_error().decode())
         self.nblocks = self.L.oracle_nblocks(self.h)
+        self.gids = sorted(gids) if gids is not None else list(range(self.nblocks))
+
+    # ---- multi-rank pieces (paper_1905_04341_b200/parallel.py) ------------------
+    def stage_compute(self, s, dt):
+        dn = C.c_double()
+        st = N.Status()
+        self._check(self.L.oracle_stage_compute(self.h, s, dt, C.byref(dn), C.byref(st)), st)
+        return dn.value, st
+
+    def exchange_dir(self, d, half):
+        self.L.oracle_exchange_dir(self.h, d, int(half))
+
+    def halo_count(self, d, side):
+        return int(self.L.oracle_halo_count(self.h, d, side))
+
+    def alloc_halo(self, n):
+        import torch
+        return torch.empty(n, dtype=torch.float64)
+
+    def halo_pack(self, gid, d, side, half, buf):
+        self.L.oracle_halo_pack(self.h, gid, d, side, int(half), C.cast(buf.data_ptr(), _dp))
+
+    def halo_unpack(self, gid, d, side, half, buf):
+        self.L.oracle_halo_unpack(self.h, gid, d, side, int(half), C.cast(buf.data_ptr(), _dp))
 
     def close(self):
         if self.h:
@@ -151,10 +188,11 @@ class OracleSolver:
                                 N.dptr(b.b3f))
         return (b, w) if with_w else b
 
-    def load_pgen(self):
-        for gid in range(self.nblocks):
+    def load_pgen(self, exchange=True):
+        for gid in self.gids:
             self.set_block(gid, self.cfg.pgen_block(gid))
-        self.exchange()
+        if exchange:
+            self.exchange()
 
     def exchange(self):
         self.L.oracle_exchange(self.h)

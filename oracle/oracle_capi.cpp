@@ -11,6 +11,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "pmhd_oracle.hpp"
 
@@ -34,12 +35,30 @@ struct MeshBase {
   virtual void diag(int kind, double* out) = 0;
   virtual void face_data(int gid, int dir, double* out) = 0;
   virtual void emf_data(int gid, int comp, double* out) = 0;
+  virtual void stage_nx(int s, double dt, std::atomic<long long>* bad, std::atomic<long long>* nf) = 0;
+  virtual void sweep(int dir, bool half) = 0;
+  virtual size_t halo_count(int dir, int side) const = 0;
+  virtual size_t pack(int gid, int dir, int side, bool half, double* out) = 0;
+  virtual size_t unpack(int gid, int dir, int side, bool half, const double* in) = 0;
+  virtual int local_of(int gid) const = 0;
 };
 
 template <class R>
 struct MeshImpl final : MeshBase {
   Mesh<R> m;
-  explicit MeshImpl(const pmhd_mesh_desc& d) : m(d) {}
+  MeshImpl(const pmhd_mesh_desc& d, std::vector<int> gids) : m(d, std::move(gids)) {}
+  void stage_nx(int s, double dt, std::atomic<long long>* bad, std::atomic<long long>* nf) override {
+    m.stage(s, dt, bad, nf, false);
+  }
+  void sweep(int dir, bool half) override { m.sweep(dir, half); }
+  size_t halo_count(int dir, int side) const override { return m.halo_count(dir, side); }
+  size_t pack(int gid, int dir, int side, bool half, double* out) override {
+    return m.pack(gid, dir, side, half, out);
+  }
+  size_t unpack(int gid, int dir, int side, bool half, const double* in) override {
+    return m.unpack(gid, dir, side, half, in);
+  }
+  int local_of(int gid) const override { return m.local_of[gid]; }
   const oracle::Geometry& geom() const override { return m.g; }
 
   static void load(oracle::Field<R>& f, const double* src) {
@@ -51,13 +70,13 @@ struct MeshImpl final : MeshBase {
 
   void set_block(int gid, const double* u, const double* b1, const double* b2,
                  const double* b3) override {
-    auto& S = m.blocks[gid].A;
+    auto& S = m.blocks[m.local_of[gid]].A;
     const size_t nc = S.u[0].a.size();
     for (int v = 0; v < oracle::NHYDRO; ++v) load(S.u[v], u + v * nc);
     load(S.b1, b1); load(S.b2, b2); load(S.b3, b3);
   }
   void get_block(int gid, double* u, double* w, double* b1, double* b2, double* b3) override {
-    auto& B = m.blocks[gid];
+    auto& B = m.blocks[m.local_of[gid]];
     auto& S = B.A;
     const auto& g = m.g;
     const size_t nc = S.u[0].a.size();
@@ -120,12 +139,12 @@ struct MeshImpl final : MeshBase {
     }
   }
   void face_data(int gid, int dir, double* out) override {
-    const auto& B = m.blocks[gid];
+    const auto& B = m.blocks[m.local_of[gid]];
     const size_t nf = B.fx[dir][0].a.size();
     for (int v = 0; v < 8; ++v) store(B.fx[dir][v], out + v * nf);
   }
   void emf_data(int gid, int comp, double* out) override {
-    const auto& B = m.blocks[gid];
+    const auto& B = m.blocks[m.local_of[gid]];
     store(comp == 0 ? B.e1 : (comp == 1 ? B.e2 : B.e3), out);
   }
 };
@@ -155,11 +174,15 @@ extern "C" {
 
 const char* oracle_last_error(void) { return g_err.c_str(); }
 
-int oracle_mesh_create(const pmhd_mesh_desc* d, int counting, int workers, oracle_mesh** out) {
+// gids / n_local: the blocks this (rank's) mesh owns; n_local <= 0: all.
+int oracle_mesh_create_local(const pmhd_mesh_desc* d, int counting, int workers, const int* gids,
+                             int n_local, oracle_mesh** out) {
   try {
+    std::vector<int> g;
+    for (int b = 0; b < n_local; ++b) g.push_back(gids[b]);
     auto* m = new oracle_mesh;
-    if (counting) m->impl.reset(new MeshImpl<Counting>(*d));
-    else m->impl.reset(new MeshImpl<double>(*d));
+    if (counting) m->impl.reset(new MeshImpl<Counting>(*d, g));
+    else m->impl.reset(new MeshImpl<double>(*d, g));
     m->counting = counting != 0;
     oracle::g_workers = counting ? 1 : (workers < 1 ? 1 : workers);
     *out = m;
@@ -173,7 +196,39 @@ int oracle_mesh_create(const pmhd_mesh_desc* d, int counting, int workers, oracl
   }
 }
 
+int oracle_mesh_create(const pmhd_mesh_desc* d, int counting, int workers, oracle_mesh** out) {
+  return oracle_mesh_create_local(d, counting, workers, nullptr, 0, out);
+}
+
 void oracle_mesh_destroy(oracle_mesh* m) { delete m; }
+
+int oracle_is_local(oracle_mesh* m, int gid) {
+  return (gid >= 0 && gid < m->impl->geom().nblocks && m->impl->local_of(gid) >= 0) ? 1 : 0;
+}
+
+// Multi-rank pieces: a stage without its trailing exchange, one local sweep,
+// and pack/unpack of the halo slabs facing remote neighbours.
+// half = 1 selects the u^{n+1/2} state (after stage 1), 0 the u^n state.
+int oracle_stage_compute(oracle_mesh* m, int stage, double dt, double* dt_next, pmhd_status* st) {
+  if (stage != 1 && stage != 2) { g_err = "stage must be 1 or 2"; return PMHD_ERR_INPUT; }
+  std::atomic<long long> bad{LLONG_MAX}, nf{0};
+  m->impl->stage_nx(stage, dt, &bad, &nf);
+  if (stage == 2 && dt_next) *dt_next = m->impl->dt_after_stage2();
+  fill_status(m->impl->geom(), bad.load(), stage, nf.load(), st);
+  return bad.load() == LLONG_MAX ? PMHD_OK : PMHD_ERR_UNPHYSICAL;
+}
+int oracle_exchange_dir(oracle_mesh* m, int dir, int half) { m->impl->sweep(dir, half != 0); return PMHD_OK; }
+long long oracle_halo_count(oracle_mesh* m, int dir, int side) { return (long long)m->impl->halo_count(dir, side); }
+int oracle_halo_pack(oracle_mesh* m, int gid, int dir, int side, int half, double* out) {
+  if (!oracle_is_local(m, gid)) { g_err = "block not local"; return PMHD_ERR_INPUT; }
+  m->impl->pack(gid, dir, side, half != 0, out);
+  return PMHD_OK;
+}
+int oracle_halo_unpack(oracle_mesh* m, int gid, int dir, int side, int half, const double* in) {
+  if (!oracle_is_local(m, gid)) { g_err = "block not local"; return PMHD_ERR_INPUT; }
+  m->impl->unpack(gid, dir, side, half != 0, in);
+  return PMHD_OK;
+}
 
 void oracle_set_workers(int workers) { oracle::g_workers = workers < 1 ? 1 : workers; }
 
@@ -184,17 +239,22 @@ int oracle_block_dims(oracle_mesh* m, int n[3]) {
 }
 
 int oracle_nblocks(oracle_mesh* m) { return m->impl->geom().nblocks; }
+int oracle_nlocal(oracle_mesh* m) {
+  int n = 0;
+  for (int g = 0; g < m->impl->geom().nblocks; ++g) n += (m->impl->local_of(g) >= 0);
+  return n;
+}
 
 int oracle_set_block(oracle_mesh* m, int gid, const double* u, const double* b1, const double* b2,
                      const double* b3) {
-  if (gid < 0 || gid >= m->impl->geom().nblocks) { g_err = "bad gid"; return PMHD_ERR_INPUT; }
+  if (!oracle_is_local(m, gid)) { g_err = "bad gid"; return PMHD_ERR_INPUT; }
   m->impl->set_block(gid, u, b1, b2, b3);
   return PMHD_OK;
 }
 
 int oracle_get_block(oracle_mesh* m, int gid, double* u, double* w, double* b1, double* b2,
                      double* b3) {
-  if (gid < 0 || gid >= m->impl->geom().nblocks) { g_err = "bad gid"; return PMHD_ERR_INPUT; }
+  if (!oracle_is_local(m, gid)) { g_err = "bad gid"; return PMHD_ERR_INPUT; }
   m->impl->get_block(gid, u, w, b1, b2, b3);
   return PMHD_OK;
 }

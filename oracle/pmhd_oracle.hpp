@@ -511,15 +511,23 @@ class Mesh {
   Geometry g;
   Phys ph;
   double cfl;
-  std::vector<Block<R>> blocks;
+  std::vector<Block<R>> blocks;      // the blocks this rank owns, in gid order
+  std::vector<int> local_of;         // gid -> index in blocks, -1 if remote
   long long floor_count = 0;
 
-  explicit Mesh(const pmhd_mesh_desc& d) : g(d), ph(d), cfl(d.cfl) {
-    blocks.resize(g.nblocks);
-    for (int b = 0; b < g.nblocks; ++b) {
-      Block<R>& B = blocks[b];
-      B.gid = b;
-      g.block_coords(b, B.c);
+  // gids: the blocks this rank owns (all blocks when empty).
+  explicit Mesh(const pmhd_mesh_desc& d, std::vector<int> gids = {}) : g(d), ph(d), cfl(d.cfl) {
+    if (gids.empty())
+      for (int b = 0; b < g.nblocks; ++b) gids.push_back(b);
+    std::sort(gids.begin(), gids.end());
+    local_of.assign(g.nblocks, -1);
+    blocks.resize(gids.size());
+    for (size_t lb = 0; lb < gids.size(); ++lb) {
+      if (gids[lb] < 0 || gids[lb] >= g.nblocks) throw ConfigErr("gid out of range");
+      local_of[gids[lb]] = int(lb);
+      Block<R>& B = blocks[lb];
+      B.gid = gids[lb];
+      g.block_coords(B.gid, B.c);
       B.A.alloc(g); B.B.alloc(g);
       for (auto& f : B.w) f.resize(g.n[2], g.n[1], g.n[0]);
       for (auto& f : B.wend) f.resize(g.n[2], g.n[1], g.n[0]);
@@ -770,35 +778,98 @@ class Mesh {
     for (int dir = 0; dir < g.dim; ++dir) sweep(dir, use_B);
   }
 
+  // Ghost range that block side r receives in direction dir, for array v
+  // (0..4 cells, 5..7 faces b1f..b3f): [q0, q1) along dir.  The sender's
+  // range is the same shifted by +m (r = 0, from the lower neighbour) or -m.
+  void recv_range(int dir, int r, int v, int* q0, int* q1) const {
+    const int ng = g.ng, s = (dir == 0) ? g.is : (dir == 1 ? g.js : g.ks), e = s + g.mb[dir];
+    const bool normal = (v == 5 + dir);
+    if (r == 0) { *q0 = 0; *q1 = normal ? s + 1 : ng; }
+    else { *q0 = normal ? e + 1 : e; *q1 = e + ng + (normal ? 1 : 0); }
+  }
+  static Field<R>& field(State<R>& S, int v) { return v < 5 ? S.u[v] : (v == 5 ? S.b1 : (v == 6 ? S.b2 : S.b3)); }
+  static const Field<R>& field(const State<R>& S, int v) {
+    return v < 5 ? S.u[v] : (v == 5 ? S.b1 : (v == 6 ? S.b2 : S.b3));
+  }
+  int neighbour(const Block<R>& blk, int dir, int side) const {
+    int c[3] = {blk.c[0], blk.c[1], blk.c[2]};
+    c[dir] += side ? 1 : -1;
+    return g.gid_of(c);
+  }
+
+  // One sweep over the blocks whose neighbour is local; ghosts facing a
+  // remote neighbour are left for unpack().
   void sweep(int dir, bool use_B) {
-    const int ng = g.ng, m = g.mb[dir];
-    const int s = (dir == 0) ? g.is : (dir == 1 ? g.js : g.ks);
-    const int e = s + m;
+    const int m = g.mb[dir];
     for (auto& blk : blocks) {
-      int cl[3] = {blk.c[0], blk.c[1], blk.c[2]}, cu[3] = {blk.c[0], blk.c[1], blk.c[2]};
-      cl[dir] -= 1; cu[dir] += 1;
-      const Block<R>& lo = blocks[g.gid_of(cl)];
-      const Block<R>& hi = blocks[g.gid_of(cu)];
       State<R>& D = use_B ? blk.B : blk.A;
-      const State<R>& L = use_B ? lo.B : lo.A;
-      const State<R>& H = use_B ? hi.B : hi.A;
-      auto cell_copy = [&](Field<R>& dst, const Field<R>& sl, const Field<R>& sh) {
-        copy_slab(dst, sl, dir, 0, ng, m);          // lower ghosts <- lower neighbour
-        copy_slab(dst, sh, dir, e, e + ng, -m);     // upper ghosts <- upper neighbour
-      };
-      for (int v = 0; v < NHYDRO; ++v) cell_copy(D.u[v], L.u[v], H.u[v]);
-      Field<R>* df[3] = {&D.b1, &D.b2, &D.b3};
-      const Field<R>* lf[3] = {&L.b1, &L.b2, &L.b3};
-      const Field<R>* hf[3] = {&H.b1, &H.b2, &H.b3};
-      for (int f = 0; f < 3; ++f) {
-        if (f == dir) {
-          copy_slab(*df[f], *lf[f], dir, 0, s + 1, m);
-          copy_slab(*df[f], *hf[f], dir, e + 1, e + ng + 1, -m);
-        } else {
-          cell_copy(*df[f], *lf[f], *hf[f]);
+      for (int r = 0; r < 2; ++r) {
+        const int ln = local_of[neighbour(blk, dir, r)];
+        if (ln < 0) continue;
+        const State<R>& N = use_B ? blocks[ln].B : blocks[ln].A;
+        for (int v = 0; v < 8; ++v) {
+          int q0, q1;
+          recv_range(dir, r, v, &q0, &q1);
+          copy_slab(field(D, v), field(N, v), dir, q0, q1, r == 0 ? m : -m);
         }
       }
     }
+  }
+
+  // pack_boundary: the slab block gid sends to its neighbour
+  // on `side` in direction dir; variable-major (u0..u4, b1f, b2f, b3f), each
+  // slab in k-j-i order with i fastest.  Returns the element count.
+  template <class Fn>
+  static void for_slab(const Field<R>& f, int dir, int q0, int q1, Fn&& fn) {
+    const int kb = (dir == 2) ? q0 : 0, kend = (dir == 2) ? q1 : f.n3;
+    const int jb = (dir == 1) ? q0 : 0, jend = (dir == 1) ? q1 : f.n2;
+    const int ib = (dir == 0) ? q0 : 0, iend = (dir == 0) ? q1 : f.n1;
+    for (int k = kb; k < kend; ++k)
+      for (int j = jb; j < jend; ++j)
+        for (int i = ib; i < iend; ++i) fn(k, j, i);
+  }
+  size_t pack(int gid, int dir, int side, bool use_B, double* out) {
+    const Block<R>& blk = blocks[local_of[gid]];
+    const State<R>& S = use_B ? blk.B : blk.A;
+    const int r = 1 - side, m = g.mb[dir];
+    size_t n = 0;
+    for (int v = 0; v < 8; ++v) {
+      int q0, q1;
+      recv_range(dir, r, v, &q0, &q1);
+      const int sh = (r == 0) ? m : -m;  // receiver q <- sender q + sh
+      const Field<R>& f = field(S, v);
+      for_slab(f, dir, q0 + sh, q1 + sh, [&](int k, int j, int i) { out[n++] = value_of(f(k, j, i)); });
+    }
+    return n;
+  }
+  // unpack_boundary: ghosts of block gid on `side` (0 lower,
+  // 1 upper) from the neighbour's pack(..., 1 - side).
+  size_t unpack(int gid, int dir, int side, bool use_B, const double* in) {
+    Block<R>& blk = blocks[local_of[gid]];
+    State<R>& S = use_B ? blk.B : blk.A;
+    size_t n = 0;
+    for (int v = 0; v < 8; ++v) {
+      int q0, q1;
+      recv_range(dir, side, v, &q0, &q1);
+      Field<R>& f = field(S, v);
+      for_slab(f, dir, q0, q1, [&](int k, int j, int i) { f(k, j, i) = R(in[n++]); });
+    }
+    return n;
+  }
+  size_t halo_count(int dir, int side) const {
+    size_t n = 0;
+    const int ext[8][3] = {{g.n[0], g.n[1], g.n[2]}, {g.n[0], g.n[1], g.n[2]}, {g.n[0], g.n[1], g.n[2]},
+                           {g.n[0], g.n[1], g.n[2]}, {g.n[0], g.n[1], g.n[2]},
+                           {g.n[0] + 1, g.n[1], g.n[2]}, {g.n[0], g.n[1] + 1, g.n[2]},
+                           {g.n[0], g.n[1], g.n[2] + 1}};
+    for (int v = 0; v < 8; ++v) {
+      int q0, q1;
+      recv_range(dir, side, v, &q0, &q1);
+      size_t t = 1;
+      for (int a = 0; a < 3; ++a) t *= (a == dir) ? size_t(q1 - q0) : size_t(ext[v][a]);
+      n += t;
+    }
+    return n;
   }
 
   // dst[idx_dir = q] = src[q + off] for q in [q0, q1), all other indices full.
@@ -816,7 +887,8 @@ class Mesh {
   // One VL2 stage.  Stage 1: B = A - (dt/2) L_donor(A).
   // Stage 2: A = A - dt L_plm(B).  Then exchange the result.  *bad receives
   // the smallest failing global cell key (unchanged if none).
-  void stage(int s, double dt, std::atomic<long long>* bad, std::atomic<long long>* nfloor) {
+  void stage(int s, double dt, std::atomic<long long>* bad, std::atomic<long long>* nfloor,
+             bool do_exchange = true) {
     for (auto& B : blocks) {
       const State<R>& in = (s == 1) ? B.A : B.B;
       c2p_all(B, in, bad);
@@ -825,7 +897,7 @@ class Mesh {
       State<R>& out = (s == 1) ? B.B : B.A;
       update(B, B.A, out, (s == 1) ? 0.5 : 1.0, dt, bad, nfloor);
     }
-    exchange(s == 1);
+    if (do_exchange) exchange(s == 1);
   }
 
   // dt after stage 2 (from the end-of-stage primitives), CFL * min.

@@ -58,6 +58,16 @@ struct KStage {
   int in_sel, out_sel, stage, plm;  // base is always st[0]
 };
 
+// One halo slab message: per array v, its origin and extents (i, j, k) and its
+// offset in the contiguous buffer (off[8] = total doubles).
+struct HaloSlab {
+  int org[8][3];
+  int ext[8][3];
+  long long off[9];
+};
+void launch_halo_copy(double* const* dev_arrays, const KGeom& G, const HaloSlab& sl, double* buf,
+                      int to_buf, cudaStream_t s);
+
 // Launchers (kernels.cu).
 void launch_c2p_all(const DevBlock* blks, const KGeom& G, const KPhys& ph, int sel, DevRed* red,
                     int stage, cudaStream_t s);
@@ -72,6 +82,7 @@ void launch_update(const DevBlock* blks, const KGeom& G, const KStage& ks, cudaS
 void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                     DevRed* red, int want_dt, cudaStream_t s);
 void launch_exchange(const DevBlock* blks, const KGeom& G, int sel, cudaStream_t s);
+void launch_exchange_dir(const DevBlock* blks, const KGeom& G, int sel, int dir, cudaStream_t s);
 void launch_dt_from_state(const DevBlock* blks, const KGeom& G, const KPhys& ph, DevRed* red,
                           cudaStream_t s);
 void launch_divb(const DevBlock* blks, const KGeom& G, DevRed* red, cudaStream_t s);

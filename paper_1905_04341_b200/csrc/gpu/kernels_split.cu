@@ -341,6 +341,7 @@ __global__ void k_exchange(const DevBlock* __restrict__ blks, KGeom G, int sel) 
     else { q = e + 1 + (l - ng - 1); qs = q - m; nb = blks[b].nbr[DIR][1]; }
   }
   (void)s;
+  if (nb < 0) return;  // remote neighbour: filled by halo unpack
   long long dst, src;
   if (DIR == 0) { dst = G.idx(a, c, q); src = G.idx(a, c, qs); }
   else if (DIR == 1) { dst = G.idx(a, q, c); src = G.idx(a, qs, c); }
@@ -392,7 +393,11 @@ void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const
 }
 
 void launch_exchange(const DevBlock* blks, const KGeom& G, int sel, cudaStream_t s) {
-  for (int dir = 0; dir < G.dim; ++dir) {
+  for (int dir = 0; dir < G.dim; ++dir) launch_exchange_dir(blks, G, sel, dir, s);
+}
+
+void launch_exchange_dir(const DevBlock* blks, const KGeom& G, int sel, int dir, cudaStream_t s) {
+  {
     long long plane;
     if (dir == 0) plane = (long long)(G.n3 + 1) * (G.n2 + 1);
     else if (dir == 1) plane = (long long)(G.n3 + 1) * (G.n1 + 1);

@@ -51,7 +51,9 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
 
   // ---- P1: cell-centred E of the stage-input state ------------------------
   const int npl = d3 ? 3 : 1;
-  for (int q = tid; q < npl * EY * EX; q += UTHR) {
+#pragma unroll
+  for (int q = tid; q < 3 * EY * EX; q += UTHR) {
+    if (q >= npl * EY * EX) break;
     const int c = q % EX, r = (q / EX) % EY, pl = q / (EX * EY);
     const int ii = i0 - 1 + c, jj = j0 - 1 + r, kk = d3 ? k - 1 + pl : k;
     const int ps = d3 ? pl : 1;
@@ -66,6 +68,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
 
   // ---- P2: corner EMFs -------------------------------------------------------
   const int mode = ph.emf;
+#pragma unroll
   for (int q = tid; q < (UY + 1) * (UX + 1); q += UTHR) {  // E3 at plane k
     const int c = q % (UX + 1), r = q / (UX + 1);
     if (c > nx || r > ny) continue;
@@ -76,6 +79,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
                            ec[2][1][ec_r][ec_c - 1], ec[2][1][ec_r - 1][ec_c],
                            ec[2][1][ec_r - 1][ec_c - 1]);
   }
+#pragma unroll
   for (int q = tid; q < 2 * (UY + 1) * UX; q += UTHR) {  // E1 at k-1/2, k+1/2
     const int c = q % UX, r = (q / UX) % (UY + 1), h = q / (UX * (UY + 1));
     if (c >= nx || r > ny) continue;
@@ -92,6 +96,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
     }
     e1s[h][r][c] = e;
   }
+#pragma unroll
   for (int q = tid; q < 2 * UY * (UX + 1); q += UTHR) {  // E2 at k-1/2, k+1/2
     const int c = q % (UX + 1), r = (q / (UX + 1)) % UY, h = q / ((UX + 1) * UY);
     if (c > nx || r >= ny) continue;

@@ -21,7 +21,7 @@
 using namespace pmhd_gpu;
 
 #ifndef PMHD_VARIANT
-#define PMHD_VARIANT "split"
+#define PMHD_VARIANT "fused(flux x3 + update) [PMHD_KERNELS=split: one kernel per op]"
 #endif
 #ifdef PMHD_PARITY
 #define PMHD_BUILD_INFO PMHD_VARIANT "+parity(fmad=false)"
@@ -128,7 +128,7 @@ void rec(pmhd_mesh* m, int slot) {
 }
 
 // Enqueue one VL2 stage (no synchronization unless profiling).
-int enqueue_stage(pmhd_mesh* m, int s, double dt) {
+int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true) {
   pmhd_ctx* ctx = m->ctx;
   const KGeom& G = m->G;
   const double beta = (s == 1) ? 0.5 : 1.0;
@@ -162,9 +162,9 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt) {
     launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
   }
   rec(m, 4);
-  launch_exchange(m->dblk, G, ks.out_sel, st);
+  if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st);
   rec(m, 5);
-  m->times.kernel_launches += (m->variant == 0) ? 1 + 2 * G.dim : 4 + 2 * G.dim;
+  m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim : 4 + G.dim) + (do_exchange ? G.dim : 0);
   CK(cudaGetLastError());
   if (s == 2) {  // u^{n+1} (st[2]) becomes the current state: flip the tables
     std::swap(m->hblk, m->hblk_alt);
@@ -348,7 +348,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
         const int ng = (c[2] * nb[1] + c[1]) * nb[0] + c[0];
         int li = -1;
         for (int q = 0; q < G.nb; ++q) if (m->gids[q] == ng) { li = q; break; }
-        if (li < 0) { m->all_local = false; li = b; }
+        if (li < 0) m->all_local = false;  // remote: ghosts come from halo unpack
         B.nbr[d][side] = li;
       }
   }
@@ -581,6 +581,86 @@ int pmhd_gpu_diag(pmhd_mesh* m, int kind, double* out) {
     return PMHD_OK;
   }
   return fail(ctx, PMHD_ERR_INPUT, "unknown diagnostic");
+}
+
+//------------------------------------------------------------- multi-rank pieces
+namespace {
+// Ghost range [q0, q1) along dir that side r (0 lower, 1 upper) receives for
+// array v (0..4 cells, 5..7 faces); same as the oracle's recv_range.
+void recv_range(const KGeom& G, int dir, int r, int v, int* q0, int* q1) {
+  const int ng = G.ng, s = G.ng, e = s + G.mb[dir];
+  const bool normal = (v == 5 + dir);
+  if (r == 0) { *q0 = 0; *q1 = normal ? s + 1 : ng; }
+  else { *q0 = normal ? e + 1 : e; *q1 = e + ng + (normal ? 1 : 0); }
+}
+// Slab of block-side `side`: send=true -> what this block sends to that
+// neighbour; send=false -> the ghosts it receives from it.
+HaloSlab make_slab(const KGeom& G, int dir, int side, bool send) {
+  HaloSlab sl;
+  const int r = send ? 1 - side : side;
+  const int sh = send ? ((r == 0) ? G.mb[dir] : -G.mb[dir]) : 0;
+  long long off = 0;
+  for (int v = 0; v < 8; ++v) {
+    const int ext[3] = {G.n1 + (v == 5), G.n2 + (v == 6), G.n3 + (v == 7)};
+    int q0, q1;
+    recv_range(G, dir, r, v, &q0, &q1);
+    for (int a = 0; a < 3; ++a) {
+      sl.org[v][a] = (a == dir) ? q0 + sh : 0;
+      sl.ext[v][a] = (a == dir) ? q1 - q0 : ext[a];
+    }
+    sl.off[v] = off;
+    off += (long long)sl.ext[v][0] * sl.ext[v][1] * sl.ext[v][2];
+  }
+  sl.off[8] = off;
+  return sl;
+}
+}  // namespace
+
+int pmhd_gpu_stage_compute(pmhd_mesh* m, int stage, double dt, double* dt_next, pmhd_status* st) {
+  if (!m) return PMHD_ERR_INPUT;
+  if (stage != 1 && stage != 2) return fail(m->ctx, PMHD_ERR_INPUT, "stage must be 1 or 2");
+  int rc = reset_red(m);
+  if (!rc) rc = enqueue_stage(m, stage, dt, false);
+  if (rc) return rc;
+  return finish(m, stage, stage, stage == 2 ? dt_next : nullptr, st);
+}
+
+int pmhd_gpu_exchange_dir(pmhd_mesh* m, int dir, int half) {
+  if (!m || dir < 0 || dir >= m->G.dim) return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  launch_exchange_dir(m->dblk, m->G, half ? 1 : 0, dir, ctx->stream);
+  m->times.kernel_launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PMHD_OK;
+}
+
+int pmhd_gpu_halo_count(const pmhd_mesh* m, int dir, int side, long long* n) {
+  if (!m || !n || dir < 0 || dir >= m->G.dim || side < 0 || side > 1) return PMHD_ERR_INPUT;
+  *n = make_slab(m->G, dir, side, false).off[8];
+  return PMHD_OK;
+}
+
+static int halo_xfer(pmhd_mesh* m, int gid, int dir, int side, int half, double* dev_buf, bool pack) {
+  if (!m || !dev_buf || dir < 0 || dir >= m->G.dim || side < 0 || side > 1) return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  const int b = local_index(m, gid);
+  if (b < 0) return fail(ctx, PMHD_ERR_INPUT, "block not local");
+  const HaloSlab sl = make_slab(m->G, dir, side, pack);
+  double* const* arrays = &m->dblk[b].st[half ? 1 : 0][0];  // device address of the 8 pointers
+  launch_halo_copy(arrays, m->G, sl, dev_buf, pack ? 1 : 0, ctx->stream);
+  m->times.kernel_launches += 1;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PMHD_OK;
+}
+
+int pmhd_gpu_halo_pack(pmhd_mesh* m, int gid, int dir, int side, int half, double* dev_buf) {
+  return halo_xfer(m, gid, dir, side, half, dev_buf, true);
+}
+
+int pmhd_gpu_halo_unpack(pmhd_mesh* m, int gid, int dir, int side, int half, const double* dev_buf) {
+  return halo_xfer(m, gid, dir, side, half, const_cast<double*>(dev_buf), false);
 }
 
 int pmhd_gpu_set_profiling(pmhd_mesh* m, int on) {

@@ -147,7 +147,8 @@ GPU_SYMBOLS = [
     "pmhd_gpu_block_dims", "pmhd_gpu_upload_block", "pmhd_gpu_download_block",
     "pmhd_gpu_exchange", "pmhd_gpu_new_dt", "pmhd_gpu_stage", "pmhd_gpu_vl2_step",
     "pmhd_gpu_run", "pmhd_gpu_diag", "pmhd_gpu_set_profiling", "pmhd_gpu_region_times",
-    "pmhd_gpu_build_info", "pmhd_gpu_stream",
+    "pmhd_gpu_build_info", "pmhd_gpu_stream", "pmhd_gpu_stage_compute", "pmhd_gpu_exchange_dir",
+    "pmhd_gpu_halo_count", "pmhd_gpu_halo_pack", "pmhd_gpu_halo_unpack",
 ]
 
 
@@ -187,6 +188,11 @@ def gpu_lib(parity: bool = False) -> C.CDLL:
         L.pmhd_gpu_diag.argtypes = [C.c_void_p, C.c_int, _dp]
         L.pmhd_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
         L.pmhd_gpu_region_times.argtypes = [C.c_void_p, _P(RegionTimes), C.c_int]
+        L.pmhd_gpu_stage_compute.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, _P(Status)]
+        L.pmhd_gpu_exchange_dir.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.pmhd_gpu_halo_count.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_longlong)]
+        L.pmhd_gpu_halo_pack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.pmhd_gpu_halo_unpack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.pmhd_gpu_stream.argtypes = [C.c_void_p]
         L.pmhd_gpu_stream.restype = C.c_void_p
         L.pmhd_gpu_build_info.argtypes = []

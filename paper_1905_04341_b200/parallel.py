@@ -1,0 +1,199 @@
+"""Multi-rank VL2 driver: one process per GPU, MeshBlocks sharded over ranks.
+
+The path shards by MeshBlock.  Its real
+exchange steps are (1) the ghost + face-B halo after every stage and (2) the
+dt minimum after stage 2.  This module is the host-side plan
+for both:
+
+* ``partition``: compact bricks of blocks per rank;
+* ``HaloPlan``: for every local block face, the neighbour block and its owner;
+* ``DistributedVL2``: a stage = engine.stage_compute + for each direction
+  (x1, x2, x3, in the order of exchange_ghosts' sweeps):
+  local sweep + pack -> transport -> unpack of the slabs that cross a rank
+  boundary; then an all-reduce(min) of dt.  With the sweeps kept sequential,
+  the result is bit-identical to the single-process exchange.
+
+Transports: ``TorchDistTransport`` (torch.distributed P2P; NCCL over NVLink
+for CUDA buffers, gloo for CPU buffers) and ``LoopbackTransport`` (several
+engines in one process, used to test the GPU pack/unpack path on one GPU
+without kernels that wait on each other).
+
+An *engine* is ``solver.GpuSolver`` (product) or, in tests only, the CPU
+oracle binding; both expose stage_compute / exchange_dir / halo_count /
+alloc_halo / halo_pack / halo_unpack / gids.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+
+def _factor(n):
+    f, p = [], 2
+    while n > 1:
+        while n % p == 0:
+            f.append(p)
+            n //= p
+        p += 1
+    return f
+
+
+def partition(nb, nranks):
+    """Split a block grid nb = (nb1, nb2, nb3) into nranks compact bricks;
+    returns owners[gid] (gid = (k*nb2 + j)*nb1 + i).  Factors of nranks go to
+    the block-grid axis with the most blocks per rank left."""
+    if nranks < 1:
+        raise ValueError("nranks must be >= 1")
+    split = [1, 1, 1]
+    for p in sorted(_factor(nranks), reverse=True):
+        best = max(range(3), key=lambda a: (nb[a] // split[a]) if (nb[a] // split[a]) % p == 0 else -1)
+        if (nb[best] // split[best]) % p != 0:
+            raise ValueError(f"cannot split block grid {tuple(nb)} over {nranks} ranks")
+        split[best] *= p
+    owners = []
+    for gid in range(nb[0] * nb[1] * nb[2]):
+        c = (gid % nb[0], (gid // nb[0]) % nb[1], gid // (nb[0] * nb[1]))
+        r = [c[a] // (nb[a] // split[a]) for a in range(3)]
+        owners.append((r[2] * split[1] + r[1]) * split[0] + r[0])
+    return owners
+
+
+@dataclass
+class HaloPlan:
+    nb: tuple
+    owners: list
+    dim: int
+
+    def neighbour(self, gid, d, side):
+        nb = self.nb
+        c = [gid % nb[0], (gid // nb[0]) % nb[1], gid // (nb[0] * nb[1])]
+        c[d] = (c[d] + (1 if side else -1)) % nb[d]
+        return (c[2] * nb[1] + c[1]) * nb[0] + c[0]
+
+    def local_gids(self, rank):
+        return [g for g, o in enumerate(self.owners) if o == rank]
+
+    def messages(self, rank, d):
+        """(sends, recvs) of rank in direction d.  A message is keyed by the
+        RECEIVING block face (gid, side): sends = [(peer, key, my_gid, my_side)],
+        recvs = [(peer, key)] with key = (my_gid, my_side).  Both lists are
+        sorted by (peer, key), so a peer pair posts matching operations in the
+        same order (NCCL P2P matches in order)."""
+        sends, recvs = [], []
+        for gid in self.local_gids(rank):
+            for side in (0, 1):
+                nbr = self.neighbour(gid, d, side)
+                peer = self.owners[nbr]
+                if peer == rank:
+                    continue
+                sends.append((peer, (nbr, 1 - side), gid, side))
+                recvs.append((peer, (gid, side)))
+        sends.sort(key=lambda s: (s[0], s[1]))
+        recvs.sort()
+        return sends, recvs
+
+
+def plan_for(cfg, nranks):
+    m = cfg.desc
+    nb = (m.nx[0] // m.mb[0], m.nx[1] // m.mb[1], m.nx[2] // m.mb[2])
+    return HaloPlan(nb, partition(nb, nranks), cfg.dim)
+
+
+class TorchDistTransport:
+    """torch.distributed point-to-point + all-reduce (nccl or gloo)."""
+
+    def __init__(self, dist, group=None):
+        self.dist = dist
+        self.group = group
+
+    def exchange(self, out, inb):
+        """out / inb: lists of (peer, tensor) in posting order."""
+        ops = [self.dist.P2POp(self.dist.isend, t, p, group=self.group) for p, t in out]
+        ops += [self.dist.P2POp(self.dist.irecv, t, p, group=self.group) for p, t in inb]
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def min(self, x, device=None):
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return float(t.item())
+
+
+@dataclass
+class _Bufs:
+    send: dict = field(default_factory=dict)
+    recv: dict = field(default_factory=dict)
+
+
+class DistributedVL2:
+    """vl2_step over a rank-local engine (SPEC.md:209-217 across ranks)."""
+
+    def __init__(self, engine, plan, rank, transport, device=None):
+        self.e, self.plan, self.rank, self.tr, self.device = engine, plan, rank, transport, device
+        self.bufs = {}
+        for d in range(plan.dim):
+            sends, recvs = plan.messages(rank, d)
+            b = _Bufs()
+            for peer, key, gid, side in sends:
+                b.send[key] = engine.alloc_halo(engine.halo_count(d, 1 - side))
+            for peer, key in recvs:
+                b.recv[key] = engine.alloc_halo(engine.halo_count(d, key[1]))
+            self.bufs[d] = (sends, recvs, b)
+
+    def exchange(self, half):
+        for d in range(self.plan.dim):
+            self.e.exchange_dir(d, half)
+            sends, recvs, b = self.bufs[d]
+            for peer, key, gid, side in sends:
+                self.e.halo_pack(gid, d, side, half, b.send[key])
+            self.tr.exchange([(p, b.send[k]) for p, k, _, _ in sends], [(p, b.recv[k]) for p, k in recvs])
+            for peer, key in recvs:
+                self.e.halo_unpack(key[0], d, key[1], half, b.recv[key])
+
+    def new_dt(self):
+        return self.tr.min(self.e.new_dt(), self.device)
+
+    def vl2_step(self, dt):
+        _, s1 = self.e.stage_compute(1, dt)
+        self.exchange(half=1)
+        dn, s2 = self.e.stage_compute(2, dt)
+        self.exchange(half=0)
+        return self.tr.min(dn, self.device), (s1.floor_count + s2.floor_count)
+
+
+class LoopbackWorld:
+    """Several rank engines in ONE process, stepped in lockstep; messages are
+    handed over by device/host copies.  Nothing waits on another kernel."""
+
+    def __init__(self, engines, plan):
+        self.engines, self.plan = engines, plan
+
+    def exchange(self, half):
+        import torch
+        for d in range(self.plan.dim):
+            for e in self.engines:
+                e.exchange_dir(d, half)
+            staged = {}
+            for r, e in enumerate(self.engines):
+                sends, _ = self.plan.messages(r, d)
+                for peer, key, gid, side in sends:
+                    buf = e.alloc_halo(e.halo_count(d, 1 - side))
+                    e.halo_pack(gid, d, side, half, buf)
+                    staged[(peer, key)] = buf
+            for r, e in enumerate(self.engines):
+                _, recvs = self.plan.messages(r, d)
+                for peer, key in recvs:
+                    src = staged[(r, key)]
+                    dst = e.alloc_halo(src.numel())
+                    dst.copy_(src.to(dst.device))
+                    e.halo_unpack(key[0], d, key[1], half, dst)
+
+    def vl2_step(self, dt):
+        for e in self.engines:
+            e.stage_compute(1, dt)
+        self.exchange(half=1)
+        dts = [e.stage_compute(2, dt)[0] for e in self.engines]
+        self.exchange(half=0)
+        return min(dts)

@@ -25,6 +25,7 @@ class CudaError(RuntimeError):
 class GpuSolver:
     def __init__(self, cfg, device: int = 0, parity: bool = False, gids=None):
         self.cfg = cfg
+        self.device = device
         self.L = N.gpu_lib(parity)
         if self.L.pmhd_gpu_abi_version() != 1:
             raise CudaError("ABI version mismatch")
@@ -89,10 +90,11 @@ class GpuSolver:
                                                    N.dptr(b.b1f), N.dptr(b.b2f), N.dptr(b.b3f)))
         return (b, w) if with_w else b
 
-    def load_pgen(self):
+    def load_pgen(self, exchange=True):
         for gid in self.gids:
             self.set_block(gid, self.cfg.pgen_block(gid))
-        self.exchange()
+        if exchange:
+            self.exchange()
 
     # ---- reference ops -------------------------------------------------------------
     def exchange(self):
@@ -136,6 +138,31 @@ class GpuSolver:
         out = np.zeros(5)
         self._check(self.L.pmhd_gpu_diag(self.mesh, N.DIAG_SUMS, N.dptr(out)))
         return out
+
+    # ---- multi-rank pieces (parallel.py) ---------------------------------------
+    def stage_compute(self, s, dt):
+        dn = C.c_double()
+        st = N.Status()
+        self._check(self.L.pmhd_gpu_stage_compute(self.mesh, s, dt, C.byref(dn), C.byref(st)), st)
+        return dn.value, st
+
+    def exchange_dir(self, d, half):
+        self._check(self.L.pmhd_gpu_exchange_dir(self.mesh, d, int(half)))
+
+    def halo_count(self, d, side):
+        n = C.c_longlong()
+        self._check(self.L.pmhd_gpu_halo_count(self.mesh, d, side, C.byref(n)))
+        return n.value
+
+    def alloc_halo(self, n):
+        import torch
+        return torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def halo_pack(self, gid, d, side, half, buf):
+        self._check(self.L.pmhd_gpu_halo_pack(self.mesh, gid, d, side, int(half), C.c_void_p(buf.data_ptr())))
+
+    def halo_unpack(self, gid, d, side, half, buf):
+        self._check(self.L.pmhd_gpu_halo_unpack(self.mesh, gid, d, side, int(half), C.c_void_p(buf.data_ptr())))
 
     def set_profiling(self, on=True):
         self._check(self.L.pmhd_gpu_set_profiling(self.mesh, int(on)))

@@ -203,3 +203,33 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
     o, g, _, _, _ = run_pair(cfg, 3, parity=True)
     for gid in range(cfg.nblocks):
         assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_multirank_halo_path_bitwise(gpu_available, nranks):
+    """The multi-rank data path (stage_compute + local sweeps + halo pack /
+    unpack kernels + transport) with nranks rank-engines on ONE GPU, stepped in
+    lockstep by the host (no kernel waits on another), is bit-identical to the
+    oracle: the GPU side of SURVEY.md §8e."""
+    from paper_1905_04341_b200.parallel import plan_for, LoopbackWorld
+    kw = dict(nx1=32, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, x2max=0.5, x3max=0.5, wave_n1=1,
+              wave_n2=1, wave_amp=1e-3)
+    cfg = RunConfig(**kw)
+    plan = plan_for(cfg, nranks)
+    engines = [GpuSolver(cfg, parity=True, gids=plan.local_gids(r)) for r in range(nranks)]
+    for e in engines:
+        e.load_pgen(exchange=False)
+    world = LoopbackWorld(engines, plan)
+    world.exchange(half=0)
+    o = OracleSolver(cfg, workers=8)
+    o.load_pgen()
+    dt = o.new_dt()
+    assert min(e.new_dt() for e in engines) == dt
+    for _ in range(3):
+        dto, _ = o.vl2_step(dt)
+        dtg = world.vl2_step(dt)
+        assert dto == dtg
+        dt = dto
+    for r, e in enumerate(engines):
+        for gid in plan.local_gids(r):
+            assert np.array_equal(e.get_block(gid).u, o.get_block(gid).u), (r, gid)
