@@ -31,6 +31,10 @@ B_ALG = 320.0          # compulsory HBM bytes per cell-update
 F_ALG_FILE = os.path.join(ROOT, "profiles", "falg_counting.json")
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# PMHD_BENCH_TRANSPORT=gloo-host: run the N>1 code path with gloo + host-staged
+# halos (all ranks may share one GPU) to validate it; numbers are not
+# measurements and the JSON says so.
+GLOO_HOST = os.environ.get("PMHD_BENCH_TRANSPORT", "") == "gloo-host"
 
 
 def parse():
@@ -39,7 +43,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=256, help="cells per dimension per GPU")
+    p.add_argument("--size", type=int, default=256, help="cells per dimension per GPU")
     p.add_argument("--riemann", default="hlld")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -179,7 +183,7 @@ def run_reference(args):
     from oracle.binding import OracleSolver
     ref = os.path.exists(os.path.join(ROOT, "oracle", "_ref", "liboracle_ref.so"))
     nz = 32
-    cfg = make_config(args.n, 1, riemann=args.riemann, nz=nz)
+    cfg = make_config(args.size, 1, riemann=args.riemann, nz=nz)
     s = OracleSolver(cfg, workers=workers, ref=ref)
     s.load_pgen()
     dt = s.new_dt()
@@ -193,14 +197,14 @@ def run_reference(args):
     cells = cfg.active_cells
     tot = sum(times)
     value = cells * len(times) / tot
-    sample = (f"each step = 1 VL2 cycle of the {args.n}x{args.n}x{nz} periodic slab of the M4 linear wave "
+    sample = (f"each step = 1 VL2 cycle of the {args.size}x{args.size}x{nz} periodic slab of the M4 linear wave "
               f"(bounded sample of the 256^3 workload; identical per-cell work), CPU oracle "
               f"{'through the reference par_for/ThreadPool (oracle/_ref)' if ref else '(oracle/liboracle.so)'}")
     line = {"impl": "reference", "metric": "cell-updates/s (fp64 VL2+PLM+HLLD+CT MHD)", "value": value,
             "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (linear-wave problem generator)",
-            "config": {"workload": f"M4 linear fast wave {args.n}^3 per GPU (sampled as {args.n}x{args.n}x{nz})",
+            "config": {"workload": f"M4 linear fast wave {args.size}^3 per GPU (sampled as {args.size}x{args.size}x{nz})",
                        "riemann": args.riemann, "cells_per_step": cells},
             "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": workers, "kind": "port",
                              "sample": sample},
@@ -217,12 +221,18 @@ def run_ours(args):
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if GLOO_HOST:  # validation of the N>1 flow on one GPU (never a measurement)
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if GLOO_HOST and torch.cuda.device_count() <= local:
+        local = 0
     torch.cuda.set_device(local)
+    xdev = "cpu" if GLOO_HOST else "cuda"
     from paper_1905_04341_b200.solver import GpuSolver
     from paper_1905_04341_b200 import native as N
 
-    n = args.n
+    n = args.size
     # global (n*ws) x n x n periodic mesh, one n^3 MeshBlock per rank
     cfg = make_config(n, ws, riemann=args.riemann)
     cells_rank = n ** 3
@@ -235,7 +245,8 @@ def run_ours(args):
     g.set_block(my_gid, host)
     drv = None
     if dist is not None:
-        drv = DistributedVL2(g, plan, rank, TorchDistTransport(dist), device=f"cuda:{local}")
+        drv = DistributedVL2(g, plan, rank, TorchDistTransport(dist, host_staging=GLOO_HOST),
+                             device=f"cuda:{local}")
         drv.exchange(half=0)
     else:
         g.exchange()
@@ -244,7 +255,7 @@ def run_ours(args):
     def allreduce_min(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=xdev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         return float(t.item())
 
@@ -276,7 +287,7 @@ def run_ours(args):
     per_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     tot_ms = evs[0].elapsed_time(evs[-1])
     if dist is not None:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=xdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     value = ws * cells_rank * args.steps / (tot_ms * 1e-3)
@@ -343,7 +354,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         if dist is not None:
-            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            t = torch.tensor([ms], dtype=torch.float64, device=xdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         for a in arrs + outs:
@@ -367,13 +378,17 @@ def run_ours(args):
             "config": {"workload": f"M4 3D linear fast wave, {n}^3 active cells per GPU in one MeshBlock, "
                                    f"HLLD+PLM(MC)+CT, CFL 0.3, A=1e-6",
                        "global_cells": [n * ws, n, n], "parallelism": f"{ws} rank(s), one {n}^3 block each",
-                       "l2": "inputs larger than L2 (1.5 GB state per GPU vs 126 MB L2)",
+                       "l2": (f"inputs larger than L2 ({8 * 8 * (n + 4) ** 3 / 1e9:.2f} GB state per GPU "
+                              f"vs 126 MB L2)" if 64 * (n + 4) ** 3 > 126e6 else
+                              "state smaller than L2 (small validation size)"),
                        "statistic": "value = mean over K cycles; p80 in extra.p80_cups",
                        "variant": g.build_info},
             "p80_cups": p80,
             "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "cpu_baseline": cpu,
         }
+        if GLOO_HOST:
+            line["note"] = "PMHD_BENCH_TRANSPORT=gloo-host validation run: NOT a measurement"
         print(json.dumps(line), flush=True)
     g.close()
     if dist is not None:

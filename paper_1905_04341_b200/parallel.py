@@ -102,21 +102,39 @@ def plan_for(cfg, nranks):
 class TorchDistTransport:
     """torch.distributed point-to-point + all-reduce (nccl or gloo)."""
 
-    def __init__(self, dist, group=None):
+    def __init__(self, dist, group=None, host_staging=False):
         self.dist = dist
         self.group = group
+        # host_staging: device buffers go through host memory (gloo cannot
+        # send CUDA tensors); used to validate the multi-rank GPU path with
+        # several processes on one GPU, never for measurements.
+        self.host_staging = host_staging
 
     def exchange(self, out, inb):
         """out / inb: lists of (peer, tensor) in posting order."""
+        if self.host_staging:
+            out = [(p, t.cpu()) for p, t in out]
+            tmp = [(p, t, t.new_empty(t.shape, device="cpu")) for p, t in inb]
+            inb_x = [(p, c) for p, _, c in tmp]
+        else:
+            inb_x = inb
         ops = [self.dist.P2POp(self.dist.isend, t, p, group=self.group) for p, t in out]
-        ops += [self.dist.P2POp(self.dist.irecv, t, p, group=self.group) for p, t in inb]
+        ops += [self.dist.P2POp(self.dist.irecv, t, p, group=self.group) for p, t in inb_x]
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
+            # NCCL completes on torch's current stream; the ABI unpacks on its
+            # own stream, so make the received bytes visible first.
+            if any(t.is_cuda for _, t in inb_x):
+                import torch
+                torch.cuda.current_stream().synchronize()
+        if self.host_staging:
+            for _, t, c in tmp:
+                t.copy_(c)
 
     def min(self, x, device=None):
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device=device)
+        t = torch.tensor([x], dtype=torch.float64, device=None if self.host_staging else device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
         return float(t.item())
 
