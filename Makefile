@@ -16,7 +16,7 @@ HOSTFLAGS:= -std=c++20 -O2 -march=x86-64-v3 -fPIC -Wall -Wextra -Iinclude
 GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu $(GPUSRC)/kernels_flux.cu $(GPUSRC)/kernels_update.cu $(GPUSRC)/kernels_halo.cu
 GPU_DEPS := $(GPU_SRCS) $(wildcard $(GPUSRC)/*.cuh) include/pmhd_gpu.h
 
-all: host gpu oracle
+all: host gpu cli oracle
 
 host: $(LIB)/libpmhd_host.so
 gpu: $(LIB)/libpmhd_gpu.so $(LIB)/libpmhd_gpu_parity.so
@@ -33,6 +33,12 @@ $(LIB)/libpmhd_gpu_parity.so: $(GPU_DEPS)
 	@mkdir -p $(LIB)
 	$(NVCC) $(NVFLAGS) --fmad=false -DPMHD_PARITY -shared -o $@ $(GPU_SRCS)
 
+cli: $(PKG)/bin/pmhd
+
+$(PKG)/bin/pmhd: $(PKG)/csrc/host/pmhd_cli.cpp $(LIB)/libpmhd_host.so $(LIB)/libpmhd_gpu.so
+	@mkdir -p $(PKG)/bin
+	$(HOSTCXX) $(HOSTFLAGS) -o $@ $< -L$(LIB) -lpmhd_host -l:libpmhd_gpu.so -Wl,-rpath,'$$ORIGIN/../lib'
+
 oracle:
 	$(MAKE) -C oracle CXX=$(HOSTCXX)
 
@@ -40,7 +46,7 @@ clean:
 	rm -f $(LIB)/*.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all host gpu oracle clean
+.PHONY: all host gpu cli oracle clean exp
 
 # A/B experiment builds (bench.py honours PMHD_GPU_LIB=<path>)
 exp: $(GPU_DEPS)
