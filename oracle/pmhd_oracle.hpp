@@ -641,12 +641,15 @@ class Mesh {
   static R corner_emf(int mode, R ea_b, R ea_bm, R eb_a, R eb_am, R wa_b, R wa_bm, R wb_a,
                       R wb_am, R c_ab, R c_amb, R c_abm, R c_ambm) {
     if (mode == PMHD_EMF_ARITH) return 0.25 * ((ea_b + ea_bm) + (eb_a + eb_am));
+    // GS05 Eq. 41: avg(faces) + dy/8 [(dE/dy)_{j-3/4} - (dE/dy)_{j-1/4}] + dx/8 [...]
+    // = avg(faces) + 1/4 sum of upwinded (E_face - E_cell): exact for E
+    // quadratic along each axis (Athena++ calculate_corner_e has the same form).
     const R t0 = ea_b + ea_bm;
     const R t1 = eb_a + eb_am;
-    const R t2 = wa_b * (c_amb - eb_am) + (1.0 - wa_b) * (c_ab - eb_a);
-    const R t3 = wa_bm * (c_ambm - eb_am) + (1.0 - wa_bm) * (c_abm - eb_a);
-    const R t4 = wb_a * (c_abm - ea_bm) + (1.0 - wb_a) * (c_ab - ea_b);
-    const R t5 = wb_am * (c_ambm - ea_bm) + (1.0 - wb_am) * (c_amb - ea_b);
+    const R t2 = wa_b * (eb_am - c_amb) + (1.0 - wa_b) * (eb_a - c_ab);
+    const R t3 = wa_bm * (eb_am - c_ambm) + (1.0 - wa_bm) * (eb_a - c_abm);
+    const R t4 = wb_a * (ea_bm - c_abm) + (1.0 - wb_a) * (ea_b - c_ab);
+    const R t5 = wb_am * (ea_bm - c_ambm) + (1.0 - wb_am) * (ea_b - c_amb);
     return 0.25 * (t0 + t1 + t2 + t3 + t4 + t5);
   }
 
