@@ -10,3 +10,4 @@ for c in blast_256 turbulence_512; do
 done
 cat gpurun_out/cli/linear_wave_64/errors.csv
 ls -la gpurun_out/cli/*/
+rm -f gpurun_out/cli/*/snapshot.pmhd
