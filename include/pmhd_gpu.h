@@ -55,7 +55,8 @@ enum {
 };
 
 /* Riemann solvers (north_star: HLLD and HLLE). */
-enum { PMHD_RIEMANN_HLLD = 0, PMHD_RIEMANN_HLLE = 1 };
+enum { PMHD_RIEMANN_HLLD = 0, PMHD_RIEMANN_HLLE = 1,
+       PMHD_RIEMANN_ROE = 2 /* SPEC.md:177-185, HLLE fallback counted */ };
 /* PLM slope limiters (MC; van Leer selectable). */
 enum { PMHD_LIMITER_MC = 0, PMHD_LIMITER_VANLEER = 1 };
 /* cons->prim failure policy (SPEC.md:136 error; Athena++-style floors). */
@@ -92,6 +93,7 @@ typedef struct pmhd_status {
   int stage;              /* 1 or 2 (SPEC.md:213 stage tag); 0 = init / dt      */
   int k, j, i;            /* lexicographically smallest failing GLOBAL active cell */
   long long floor_count;  /* floor activations in this call (eos_mode FLOOR)   */
+  long long fallback_count; /* faces where Roe fell back to HLLE */
 } pmhd_status;
 
 /* Region times (Fig. 3 analogue), milliseconds accumulated since

@@ -60,7 +60,7 @@ def lib(ref: bool = False) -> C.CDLL:
         L.oracle_fast_speed.argtypes = [_dp, C.c_double, C.c_int]
         L.oracle_fast_speed.restype = C.c_double
         L.oracle_riemann.argtypes = [C.c_int, _dp, _dp, C.c_double, C.c_double, _dp]
-        L.oracle_riemann.restype = None
+        L.oracle_riemann.restype = C.c_int
         L.oracle_phys_flux.argtypes = [_dp, C.c_double, C.c_double, _dp]
         L.oracle_phys_flux.restype = None
         L.oracle_plm_slope.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int]
@@ -96,12 +96,12 @@ def fast_speed(w8, gamma, dim):
     return lib().oracle_fast_speed(pw, gamma, dim)
 
 
-def riemann(solver, wl7, wr7, bx, gamma):
+def riemann(solver, wl7, wr7, bx, gamma, with_fallback=False):
     a, pa = _arr(wl7)
     b, pb = _arr(wr7)
     out = np.zeros(7)
-    lib().oracle_riemann(N.RIEMANN[solver], pa, pb, bx, gamma, out.ctypes.data_as(_dp))
-    return out
+    fb = lib().oracle_riemann(N.RIEMANN[solver], pa, pb, bx, gamma, out.ctypes.data_as(_dp))
+    return (out, bool(fb)) if with_fallback else out
 
 
 def phys_flux(w7, bx, gamma):

@@ -31,6 +31,7 @@ struct MeshBase {
   virtual void exchange() = 0;
   virtual double new_dt(std::atomic<long long>* bad) = 0;
   virtual void stage(int s, double dt, std::atomic<long long>* bad, std::atomic<long long>* nf) = 0;
+  virtual long long take_fallbacks() = 0;
   virtual double dt_after_stage2() = 0;
   virtual void diag(int kind, double* out) = 0;
   virtual void face_data(int gid, int dir, double* out) = 0;
@@ -102,6 +103,7 @@ struct MeshImpl final : MeshBase {
   }
   void exchange() override { m.exchange(false); }
   double new_dt(std::atomic<long long>* bad) override { return oracle::value_of(m.new_dt_from_state(bad)); }
+  long long take_fallbacks() override { return m.fallbacks.exchange(0); }
   void stage(int s, double dt, std::atomic<long long>* bad, std::atomic<long long>* nf) override {
     m.stage(s, dt, bad, nf);
   }
@@ -149,9 +151,11 @@ struct MeshImpl final : MeshBase {
   }
 };
 
-void fill_status(const oracle::Geometry& g, long long bad, int stage, long long nf, pmhd_status* st) {
+void fill_status(const oracle::Geometry& g, long long bad, int stage, long long nf, pmhd_status* st,
+                 long long fb = 0) {
   if (!st) return;
   st->floor_count = nf;
+  st->fallback_count = fb;
   st->stage = stage;
   if (bad == LLONG_MAX) {
     st->code = PMHD_OK; st->k = st->j = st->i = -1;
@@ -214,7 +218,7 @@ int oracle_stage_compute(oracle_mesh* m, int stage, double dt, double* dt_next, 
   std::atomic<long long> bad{LLONG_MAX}, nf{0};
   m->impl->stage_nx(stage, dt, &bad, &nf);
   if (stage == 2 && dt_next) *dt_next = m->impl->dt_after_stage2();
-  fill_status(m->impl->geom(), bad.load(), stage, nf.load(), st);
+  fill_status(m->impl->geom(), bad.load(), stage, nf.load(), st, m->impl->take_fallbacks());
   return bad.load() == LLONG_MAX ? PMHD_OK : PMHD_ERR_UNPHYSICAL;
 }
 int oracle_exchange_dir(oracle_mesh* m, int dir, int half) { m->impl->sweep(dir, half != 0); return PMHD_OK; }
@@ -273,7 +277,7 @@ int oracle_stage(oracle_mesh* m, int stage, double dt, double* dt_next, pmhd_sta
   std::atomic<long long> bad{LLONG_MAX}, nf{0};
   m->impl->stage(stage, dt, &bad, &nf);
   if (stage == 2 && dt_next) *dt_next = m->impl->dt_after_stage2();
-  fill_status(m->impl->geom(), bad.load(), stage, nf.load(), st);
+  fill_status(m->impl->geom(), bad.load(), stage, nf.load(), st, m->impl->take_fallbacks());
   return bad.load() == LLONG_MAX ? PMHD_OK : PMHD_ERR_UNPHYSICAL;
 }
 
@@ -282,7 +286,7 @@ int oracle_vl2_step(oracle_mesh* m, double dt, double* dt_next, pmhd_status* st)
   int rc = oracle_stage(m, 1, dt, nullptr, &s1);
   if (rc != PMHD_OK) { if (st) *st = s1; return rc; }
   rc = oracle_stage(m, 2, dt, dt_next, st);
-  if (st) st->floor_count += s1.floor_count;
+  if (st) { st->floor_count += s1.floor_count; st->fallback_count += s1.fallback_count; }
   return rc;
 }
 
@@ -342,11 +346,14 @@ double oracle_fast_speed(const double* w8, double gamma, int dim) {
 
 // Riemann flux of rotated states (d, vn, vt1, vt2, p, bt1, bt2); out[0..6] =
 // flux of (d, mn, mt1, mt2, e, bt1, bt2).
-void oracle_riemann(int solver, const double* wl, const double* wr, double bx, double gamma,
-                    double* out) {
+int oracle_riemann(int solver, const double* wl, const double* wr, double bx, double gamma,
+                   double* out) {
   const oracle::Phys ph(desc_for(gamma, solver, 0));
   if (solver == PMHD_RIEMANN_HLLE) oracle::riemann_hlle(wl, wr, bx, ph, out);
-  else oracle::riemann_hlld(wl, wr, bx, ph, out);
+  else if (solver == PMHD_RIEMANN_ROE) {
+    if (!oracle::riemann_roe(wl, wr, bx, ph, out)) { oracle::riemann_hlle(wl, wr, bx, ph, out); return 1; }
+  } else oracle::riemann_hlld(wl, wr, bx, ph, out);
+  return 0;
 }
 
 double oracle_plm_slope(double qm, double q0, double qp, int limiter) {

@@ -402,6 +402,115 @@ inline void riemann_hlld(const R* wl, const R* wr, R bx, const Phys& ph, R* flx)
   }
 }
 
+// Roe flux (the paper's solver):
+// F = (F_L + F_R)/2 - R|Lambda|L (U_R - U_L)/2 with the eigensystem of the
+// flux Jacobian at the Roe state: rho = sqrt(rho_L rho_R), v and the total
+// enthalpy density-weighted, transverse B weighted by the OTHER side's
+// sqrt(rho), normal B = the face value.  The decomposition is done in
+// primitive variables (rho, vn, vt1, vt2, p, bt1, bt2) linearised at the Roe
+// state, with the Roe & Balsara (1996) eigenvector normalisation; B_t = 0 uses
+// beta = (1,1)/sqrt 2, sgn(0) = +1.  Returns false (caller falls back to HLLE
+// and counts it) when the Roe state has a^2 <= 0.
+template <class R>
+inline bool riemann_roe(const R* wl, const R* wr, R bx, const Phys& ph, R* flx) {
+  using std::sqrt; using std::fabs; using std::fmax; using std::fmin;
+  const R bxsq = bx * bx;
+  SideState<R> L, Rt;
+  side_state(wl, bx, bxsq, ph, L);
+  side_state(wr, bx, bxsq, ph, Rt);
+  const R sdl = sqrt(wl[0]), sdr = sqrt(wr[0]);
+  const R isum = 1.0 / (sdl + sdr);
+  const R d = sdl * sdr;
+  const R u = (sdl * wl[1] + sdr * wr[1]) * isum;
+  const R v = (sdl * wl[2] + sdr * wr[2]) * isum;
+  const R w = (sdl * wl[3] + sdr * wr[3]) * isum;
+  const R h = ((L.u[4] + L.pt) / sdl + (Rt.u[4] + Rt.pt) / sdr) * isum;  // Roe total enthalpy
+  const R by = (sdr * wl[5] + sdl * wr[5]) * isum;
+  const R bz = (sdr * wl[6] + sdl * wr[6]) * isum;
+  const R id = 1.0 / d;
+  const R vsq = u * u + v * v + w * w;
+  const R btsq = by * by + bz * bz;
+  const R asq = ph.gm1 * (h - 0.5 * vsq - (bxsq + btsq) * id);
+  if (!(asq > 0.0)) return false;
+  const R ca2 = bxsq * id, bt2 = btsq * id;
+  const R tsum = ca2 + bt2 + asq, tdif = ca2 + bt2 - asq;
+  const R cf2 = 0.5 * (tsum + sqrt(tdif * tdif + 4.0 * asq * bt2));
+  const R cs2 = asq * ca2 / cf2;  // c_f^2 c_s^2 = a^2 c_a^2
+  const R cf = sqrt(cf2), cs = sqrt(cs2), ca = sqrt(ca2), a = sqrt(asq);
+  R af, as;
+  const R dfs = cf2 - cs2;
+  if (!(dfs > 0.0)) {
+    af = 1.0; as = 0.0;
+  } else {
+    const R idfs = 1.0 / dfs;
+    af = sqrt(fmax(R(0.0), fmin(R(1.0), (asq - cs2) * idfs)));
+    as = sqrt(fmax(R(0.0), fmin(R(1.0), (cf2 - asq) * idfs)));
+  }
+  const R bt = sqrt(btsq);
+  R bety, betz;
+  if (bt > 0.0) {
+    const R ibt = 1.0 / bt;
+    bety = by * ibt; betz = bz * ibt;
+  } else {
+    bety = R(0.70710678118654752440); betz = R(0.70710678118654752440);
+  }
+  const R sgn = (bx >= 0.0) ? R(1.0) : R(-1.0);
+  const R sd = sqrt(d);
+  const R isd = 1.0 / sd;
+  // dW = (dW/dU) dU at the Roe state
+  R du[7];
+  for (int n = 0; n < 7; ++n) du[n] = Rt.u[n] - L.u[n];
+  const R dr = du[0];
+  const R dvx = (du[1] - u * dr) * id, dvy = (du[2] - v * dr) * id, dvz = (du[3] - w * dr) * id;
+  const R dby = du[5], dbz = du[6];
+  const R dp = ph.gm1 * (du[4] - (u * du[1] + v * du[2] + w * du[3]) + 0.5 * vsq * dr -
+                         (by * dby + bz * dbz));
+  // wave amplitudes alpha_k = l_k . dW
+  const R ia2 = 1.0 / asq;
+  const R h2a = 0.5 * ia2;
+  const R q = 0.5 * isd / a;
+  const R dvt = bety * dvy + betz * dvz;
+  const R dbt = bety * dby + betz * dbz;
+  const R tfa = af * cf * h2a * dvx, tfs = as * cs * sgn * h2a * dvt;
+  const R tfp = af * h2a * id * dp, tfb = as * q * dbt;
+  const R am_f = tfp + tfb - tfa + tfs, ap_f = tfp + tfb + tfa - tfs;
+  const R tav = 0.5 * (bety * dvz - betz * dvy);
+  const R tab = 0.5 * sgn * isd * (betz * dby - bety * dbz);
+  const R am_a = tav - tab, ap_a = tav + tab;
+  const R tsa = as * cs * h2a * dvx, tss = af * cf * sgn * h2a * dvt;
+  const R tsp = as * h2a * id * dp, tsb = af * q * dbt;
+  const R am_s = tsp - tsb - tsa - tss, ap_s = tsp - tsb + tsa + tss;
+  const R a_e = dr - dp * ia2;
+  // |lambda_k| alpha_k
+  const R wfm = fabs(u - cf) * am_f, wfp = fabs(u + cf) * ap_f;
+  const R wam = fabs(u - ca) * am_a, wap = fabs(u + ca) * ap_a;
+  const R wsm = fabs(u - cs) * am_s, wsp = fabs(u + cs) * ap_s;
+  const R we = fabs(u) * a_e;
+  // D_W = sum_k |lambda_k| alpha_k r_k (primitive right eigenvectors)
+  const R sf = wfm + wfp, ss = wsm + wsp;
+  const R Dr = d * (af * sf + as * ss) + we;
+  const R Dvx = af * cf * (wfp - wfm) + as * cs * (wsp - wsm);
+  const R tm = as * cs * sgn * (wfm - wfp) + af * cf * sgn * (wsp - wsm);
+  const R Dvy = bety * tm - betz * (wam + wap);
+  const R Dvz = betz * tm + bety * (wam + wap);
+  const R Dp = d * asq * (af * sf + as * ss);
+  const R tb = sd * a * (as * sf - af * ss);
+  const R ta = sgn * sd * (wap - wam);
+  const R Dby = bety * tb + betz * ta;
+  const R Dbz = betz * tb - bety * ta;
+  // D_U = (dU/dW) D_W
+  R D[7];
+  D[0] = Dr;
+  D[1] = u * Dr + d * Dvx;
+  D[2] = v * Dr + d * Dvy;
+  D[3] = w * Dr + d * Dvz;
+  D[4] = 0.5 * vsq * Dr + d * (u * Dvx + v * Dvy + w * Dvz) + Dp * ph.igm1 + by * Dby + bz * Dbz;
+  D[5] = Dby;
+  D[6] = Dbz;
+  for (int n = 0; n < 7; ++n) flx[n] = 0.5 * (L.f[n] + Rt.f[n]) - 0.5 * D[n];
+  return true;
+}
+
 // PLM slope: MC (monotonized central) or van Leer limiter,
 // applied componentwise to primitives.  Zero at extrema; exact on linear data.
 template <class R>
@@ -427,17 +536,22 @@ inline R plm_slope(R qm, R q0, R qp, int limiter) {
 // a pure sign(F_rho) switch flips 0 <-> 1 on round-off noise of a vanishing
 // mass flux and turns 1-ulp differences into O(dt dE) field differences.
 // c1024 = 1024 * dt / dx_dir (full-cycle dt, both stages).
+// Returns 1 when the Roe solver fell back to HLLE at this face.
 template <class R>
-inline void face_solve(const R* wl, const R* wr, R bx, const Phys& ph, double c1024, R* out) {
+inline int face_solve(const R* wl, const R* wr, R bx, const Phys& ph, double c1024, R* out) {
   using std::fmin; using std::fmax;
   R flx[7];
+  int fb = 0;
   if (ph.riemann == PMHD_RIEMANN_HLLE) riemann_hlle(wl, wr, bx, ph, flx);
-  else riemann_hlld(wl, wr, bx, ph, flx);
+  else if (ph.riemann == PMHD_RIEMANN_ROE) {
+    if (!riemann_roe(wl, wr, bx, ph, flx)) { riemann_hlle(wl, wr, bx, ph, flx); fb = 1; }
+  } else riemann_hlld(wl, wr, bx, ph, flx);
   for (int n = 0; n < 5; ++n) out[n] = flx[n];
   out[5] = -flx[5];
   out[6] = flx[6];
   const R vc = c1024 * flx[0] / (wl[0] + wr[0]);
   out[7] = 0.5 + fmax(R(-0.5), fmin(R(0.5), vc));
+  return fb;
 }
 
 //============================================================================
@@ -514,6 +628,7 @@ class Mesh {
   std::vector<Block<R>> blocks;      // the blocks this rank owns, in gid order
   std::vector<int> local_of;         // gid -> index in blocks, -1 if remote
   long long floor_count = 0;
+  std::atomic<long long> fallbacks{0};  // Roe -> HLLE fallbacks since reset
 
   // gids: the blocks this rank owns (all blocks when empty).
   explicit Mesh(const pmhd_mesh_desc& d, std::vector<int> gids = {}) : g(d), ph(d), cfl(d.cfl) {
@@ -613,7 +728,7 @@ class Mesh {
         }
       }
       R out[8];
-      face_solve(wl, wr, bn(k, j, i), ph, c1024, out);
+      if (face_solve(wl, wr, bn(k, j, i), ph, c1024, out)) fallbacks.fetch_add(1);
       B.fx[dir][IDN](k, j, i) = out[0];  // un-rotate momentum fluxes
       B.fx[dir][iv[0]](k, j, i) = out[1];
       B.fx[dir][iv[1]](k, j, i) = out[2];

@@ -48,6 +48,7 @@ struct DevRed {
   unsigned long long bad_key;     // smallest failing global cell key
   unsigned long long floor_count;
   unsigned long long divb_bits;   // max |div B| as bits
+  unsigned long long fallback_count;  // Roe -> HLLE fallbacks
 };
 
 // Stage coefficients c_d = beta*dt/dx_d, computed on the host with the same
@@ -74,10 +75,11 @@ void launch_c2p_all(const DevBlock* blks, const KGeom& G, const KPhys& ph, int s
 void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel, int plm,
                  double c1024, cudaStream_t s);
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
-                       int plm, double c1024, int stage, DevRed* red, cudaStream_t s);
+                       int plm, double c1024, int stage, DevRed* red, int slab, int nslab, int S,
+                       cudaStream_t s);
 void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s);
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
-                         DevRed* red, int want_dt, cudaStream_t s);
+                         DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s);
 void launch_update(const DevBlock* blks, const KGeom& G, const KStage& ks, cudaStream_t s);
 void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                     DevRed* red, int want_dt, cudaStream_t s);

@@ -51,7 +51,7 @@ template <int DIR>
 __global__ void __launch_bounds__(NTHR, PMHD_FLUX_MINB)
 k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024,
              int stage, DevRed* red, int write_ec, int f_i0, int f_i1, int f_s0, int f_s1, int f_t0,
-             int f_t1) {
+             int f_t1, int ty0) {
   using TS = TileShape<DIR>;
   __shared__ double sw[7][TS::NCELL];  // primitives; after phase 2: q - dq/2 (low-face value)
   __shared__ double sp[7][TS::NCELL];  // after phase 2: q + dq/2 (high-face value)
@@ -60,7 +60,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   const int b = blockIdx.z / nt;
   const int t3 = f_t0 + (int)(blockIdx.z % nt);   // k for x1/x2, j for x3
   const int fi0 = f_i0 + blockIdx.x * FX;          // first face along i
-  const int fs0 = f_s0 + blockIdx.y * FS;          // first face along the 2nd axis
+  const int fs0 = f_s0 + (ty0 + blockIdx.y) * FS;  // first face along the 2nd axis
   const DevBlock& B = blks[b];
   double* const* S = B.st[sel];
 
@@ -156,7 +156,8 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     else { i = fi; k = fs; j = t3; }
     const long long id = G.idx(k, j, i);
     double out[8];
-    face_solve(wl, wr, __ldg(S[5 + DIR] + id), ph, c1024, out);
+    if (face_solve(wl, wr, __ldg(S[5 + DIR] + id), ph, c1024, out))
+      atomicAdd(&red[stage].fallback_count, 1ULL);
     double* const* F = B.fx[DIR];
     F[0][id] = out[0];
     F[rot_var<DIR>(1)][id] = out[1];
@@ -171,8 +172,13 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 
 }  // namespace
 
+// slab / nslab / S: k-slab pipelining (pmhd_gpu.cu): slab q covers k planes
+// [ks + q S, ks + (q+1) S) of x1/x2 faces (the first slab also ks-1, the last
+// up to ke) and x3 face planes [ks + q S, ...) (the last up to ke); S is a
+// multiple of FS.  nslab = 1 is the whole block.
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
-                       int plm, double c1024, int stage, DevRed* red, cudaStream_t s) {
+                       int plm, double c1024, int stage, DevRed* red, int slab, int nslab, int S,
+                       cudaStream_t s) {
   const int d3 = (G.dim == 3) ? 1 : 0;
   // face ranges of the oracle: [lo, hi) per axis
   int i0, i1, j0, j1, k0, k1;
@@ -180,18 +186,31 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   else if (dir == 1) { k0 = G.ks - d3; k1 = G.ke + d3; j0 = G.js; j1 = G.je + 1; i0 = G.is - 1; i1 = G.ie + 1; }
   else { k0 = G.ks; k1 = G.ke + 1; j0 = G.js - 1; j1 = G.je + 1; i0 = G.is - 1; i1 = G.ie + 1; }
   const int ns0 = (dir == 2) ? k0 : j0, ns1 = (dir == 2) ? k1 : j1;
-  const int nt0 = (dir == 2) ? j0 : k0, nt1 = (dir == 2) ? j1 : k1;
+  int nt0 = (dir == 2) ? j0 : k0, nt1 = (dir == 2) ? j1 : k1;
   const int write_ec = (dir == G.dim - 1) ? 1 : 0;
-  const dim3 grid((i1 - i0 + FX - 1) / FX, (ns1 - ns0 + FS - 1) / FS, (nt1 - nt0) * G.nb);
+  int ty0 = 0, ty1 = (ns1 - ns0 + FS - 1) / FS;
+  if (nslab > 1) {
+    const bool first = (slab == 0), last = (slab == nslab - 1);
+    if (dir == 2) {  // k is the tile's second axis (face planes)
+      ty0 = slab * S / FS;
+      if (!last) ty1 = (slab + 1) * S / FS;
+    } else {         // k is the launch's third axis
+      const int a = first ? nt0 : G.ks + slab * S;
+      const int e = last ? nt1 : G.ks + (slab + 1) * S;
+      nt0 = a;
+      nt1 = e;
+    }
+  }
+  const dim3 grid((i1 - i0 + FX - 1) / FX, ty1 - ty0, (nt1 - nt0) * G.nb);
   if (dir == 0)
     k_flux_fused<0><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, i1,
-                                          ns0, ns1, nt0, nt1);
+                                          ns0, ns1, nt0, nt1, ty0);
   else if (dir == 1)
     k_flux_fused<1><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, i1,
-                                          ns0, ns1, nt0, nt1);
+                                          ns0, ns1, nt0, nt1, ty0);
   else
     k_flux_fused<2><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, i1,
-                                          ns0, ns1, nt0, nt1);
+                                          ns0, ns1, nt0, nt1, ty0);
 }
 
 }  // namespace pmhd_gpu

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(TX* TY) k_flux(const DevBlock* __restrict__ bl
     }
   }
   double out[8];
-  face_solve(wl, wr, B.st[sel][5 + DIR][id], ph, c1024, out);
+  face_solve(wl, wr, B.st[sel][5 + DIR][id], ph, c1024, out);  // (no fallback count: debug path)
   double* const* F = B.fx[DIR];
   F[0][id] = out[0];
   F[V1][id] = out[1];

@@ -24,7 +24,7 @@ constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0
 
 __global__ void __launch_bounds__(UTHR, 4)
 k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, DevRed* red,
-               int want_dt) {
+               int want_dt, int kr0, int kr1) {
   __shared__ double ec[3][3][EY][EX];      // [component][plane k-1,k,k+1][j][i]
   __shared__ double e3s[UY + 1][UX + 1];   // E3 at (k, j-1/2, i-1/2)
   __shared__ double e1s[2][UY + 1][UX];    // E1 at (k-1/2 / k+1/2, j-1/2, i)
@@ -35,9 +35,9 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   __shared__ double redbuf[UTHR / 32];
 
   const bool d3 = (G.dim == 3);
-  const int nk = G.ke - G.ks;
+  const int nk = kr1 - kr0;  // k planes [kr0, kr1) of this launch (a slab)
   const int b = blockIdx.z / nk;
-  const int k = G.ks + (int)(blockIdx.z % nk);
+  const int k = kr0 + (int)(blockIdx.z % nk);
   const int i0 = G.is + blockIdx.x * UX, j0 = G.js + blockIdx.y * UY;
   const int nx = min(UX, G.ie - i0), ny = min(UY, G.je - j0);
   const DevBlock& B = blks[b];
@@ -206,9 +206,9 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
 }  // namespace
 
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
-                         DevRed* red, int want_dt, cudaStream_t s) {
-  const dim3 grid((G.ie - G.is + UX - 1) / UX, (G.je - G.js + UY - 1) / UY, (G.ke - G.ks) * G.nb);
-  k_update_fused<<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt);
+                         DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s) {
+  const dim3 grid((G.ie - G.is + UX - 1) / UX, (G.je - G.js + UY - 1) / UY, (kr1 - kr0) * G.nb);
+  k_update_fused<<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);
 }
 
 }  // namespace pmhd_gpu

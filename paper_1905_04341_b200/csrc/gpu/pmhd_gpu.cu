@@ -7,6 +7,7 @@
 // exception crosses the ABI; errors map to the defs.hpp:36-76 families.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -32,6 +33,7 @@ using namespace pmhd_gpu;
 struct pmhd_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // update kernels of the k-slab pipeline
   std::string err;
 };
 
@@ -52,6 +54,8 @@ struct pmhd_mesh {
   bool all_local = true;
   bool prof = false;
   int variant = 0;                // 0: fused flux kernels; 1: split (debug; PMHD_KERNELS=split)
+  int slab_planes = 64;           // k-slab pipeline depth (PMHD_SLAB_PLANES, 0 = off)
+  std::vector<cudaEvent_t> slab_ev;
   cudaEvent_t ev[8] = {};
   pmhd_region_times times{};
 };
@@ -84,7 +88,8 @@ std::string validate(const pmhd_mesh_desc& d) {
     return "meshblock must have more than ng cells per dimension";
   if (!(d.gamma > 1.0)) return "gamma must be > 1";
   if (!(d.cfl > 0.0 && d.cfl < 1.0)) return "cfl must be in (0,1)";
-  if (d.riemann != PMHD_RIEMANN_HLLD && d.riemann != PMHD_RIEMANN_HLLE) return "bad riemann";
+  if (d.riemann != PMHD_RIEMANN_HLLD && d.riemann != PMHD_RIEMANN_HLLE && d.riemann != PMHD_RIEMANN_ROE)
+    return "bad riemann";
   if (d.limiter != PMHD_LIMITER_MC && d.limiter != PMHD_LIMITER_VANLEER) return "bad limiter";
   if (d.eos_mode != PMHD_EOS_ERROR && d.eos_mode != PMHD_EOS_FLOOR) return "bad eos_mode";
   if (d.emf_mode != PMHD_EMF_UPWIND && d.emf_mode != PMHD_EMF_ARITH) return "bad emf_mode";
@@ -110,6 +115,7 @@ int reset_red(pmhd_mesh* m) {
     m->hred[s].bad_key = ULLONG_MAX;
     m->hred[s].floor_count = 0;
     m->hred[s].divb_bits = 0;
+    m->hred[s].fallback_count = 0;
   }
   CK(cudaMemcpyAsync(m->dred, m->hred, 3 * sizeof(DevRed), cudaMemcpyHostToDevice, ctx->stream));
   return PMHD_OK;
@@ -143,28 +149,61 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true) {
   ks.stage = s;
   ks.plm = (s == 2);
   cudaStream_t st = ctx->stream;
-  rec(m, 0);
-  if (m->variant == 1) launch_c2p_all(m->dblk, G, m->ph, ks.in_sel, m->dred, s, st);
-  rec(m, 1);
-  for (int dir = 0; dir < G.dim; ++dir) {
-    if (m->variant == 0)
-      launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], s, m->dred, st);
-    else
-      launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], st);
+  // k-slab pipeline (fused variant, 3D, not profiling): the flux kernels of
+  // slab q+1 run on the main stream while the update kernel of slab q (which
+  // needs the faces of planes up to the first plane of slab q+1) runs on the
+  // second stream, overlapping the FP64-bound flux work with the
+  // memory-bound update work.
+  const int nk = G.ke - G.ks;
+  int S = nk, nslab = 1;
+  if (m->variant == 0 && G.dim == 3 && !m->prof && m->slab_planes > 0 && nk >= 2 * m->slab_planes) {
+    S = m->slab_planes;
+    nslab = (nk + S - 1) / S;
   }
-  rec(m, 2);
-  if (m->variant == 1) launch_emf(m->dblk, G, m->ph, st);
-  rec(m, 3);
-  if (m->variant == 0) {
-    launch_update_fused(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
+  if (nslab > 1) {
+    for (int q = 0; q < nslab; ++q) {
+      for (int dir = 0; dir < G.dim; ++dir)
+        launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], s, m->dred, q,
+                          nslab, S, st);
+      CK(cudaEventRecord(m->slab_ev[q], st));
+      if (q >= 1) {  // update slab q-1 once the flux kernels of slab q are done
+        CK(cudaStreamWaitEvent(ctx->stream2, m->slab_ev[q], 0));
+        launch_update_fused(m->dblk, G, m->ph, ks, m->dred, s == 2, G.ks + (q - 1) * S,
+                            G.ks + q * S, ctx->stream2);
+      }
+    }
+    CK(cudaStreamWaitEvent(ctx->stream2, m->slab_ev[nslab - 1], 0));
+    launch_update_fused(m->dblk, G, m->ph, ks, m->dred, s == 2, G.ks + (nslab - 1) * S, G.ke,
+                        ctx->stream2);
+    CK(cudaEventRecord(m->slab_ev[nslab], ctx->stream2));
+    CK(cudaStreamWaitEvent(st, m->slab_ev[nslab], 0));
+    if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st);
+    m->times.kernel_launches += nslab * (1 + G.dim) + (do_exchange ? G.dim : 0);
   } else {
-    launch_update(m->dblk, G, ks, st);
-    launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
+    rec(m, 0);
+    if (m->variant == 1) launch_c2p_all(m->dblk, G, m->ph, ks.in_sel, m->dred, s, st);
+    rec(m, 1);
+    for (int dir = 0; dir < G.dim; ++dir) {
+      if (m->variant == 0)
+        launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], s, m->dred, 0, 1,
+                          nk, st);
+      else
+        launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], st);
+    }
+    rec(m, 2);
+    if (m->variant == 1) launch_emf(m->dblk, G, m->ph, st);
+    rec(m, 3);
+    if (m->variant == 0) {
+      launch_update_fused(m->dblk, G, m->ph, ks, m->dred, s == 2, G.ks, G.ke, st);
+    } else {
+      launch_update(m->dblk, G, ks, st);
+      launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
+    }
+    rec(m, 4);
+    if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st);
+    rec(m, 5);
+    m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim : 4 + G.dim) + (do_exchange ? G.dim : 0);
   }
-  rec(m, 4);
-  if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st);
-  rec(m, 5);
-  m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim : 4 + G.dim) + (do_exchange ? G.dim : 0);
   CK(cudaGetLastError());
   if (s == 2) {  // u^{n+1} (st[2]) becomes the current state: flip the tables
     std::swap(m->hblk, m->hblk_alt);
@@ -192,8 +231,11 @@ int finish(pmhd_mesh* m, int stage_lo, int stage_hi, double* dt_next, pmhd_statu
   s.k = s.j = s.i = -1;
   s.stage = stage_hi;
   long long nf = 0;
+  long long fb = 0;
   for (int q = stage_lo; q <= stage_hi; ++q) nf += (long long)m->hred[q].floor_count;
+  for (int q = stage_lo; q <= stage_hi; ++q) fb += (long long)m->hred[q].fallback_count;
   s.floor_count = nf;
+  s.fallback_count = fb;
   for (int q = stage_lo; q <= stage_hi; ++q) {
     if (m->hred[q].bad_key != ULLONG_MAX) {
       s.code = PMHD_ERR_UNPHYSICAL;
@@ -248,7 +290,8 @@ int pmhd_gpu_ctx_create(int device, pmhd_ctx** out) {
   auto* ctx = new pmhd_ctx;
   ctx->device = device;
   if (cudaSetDevice(device) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return PMHD_ERR_CUDA;
   }
@@ -260,6 +303,7 @@ int pmhd_gpu_ctx_destroy(pmhd_ctx* ctx) {
   if (!ctx) return PMHD_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   delete ctx;
   return PMHD_OK;
 }
@@ -305,6 +349,8 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   }
   G.nb = int(m->gids.size());
   if (const char* kv = std::getenv("PMHD_KERNELS")) m->variant = (std::string(kv) == "split") ? 1 : 0;
+  if (const char* sp = std::getenv("PMHD_SLAB_PLANES")) m->slab_planes = std::atoi(sp);
+  if (m->slab_planes > 0) m->slab_planes = std::max(8, (m->slab_planes / 8) * 8);  // tile multiple
   m->ph.gamma = desc->gamma;
   m->ph.gm1 = desc->gamma - 1.0;
   m->ph.igm1 = 1.0 / (desc->gamma - 1.0);
@@ -366,6 +412,8 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   const size_t nrows = size_t(G.nb) * 5 * (G.ke - G.ks) * (G.je - G.js);
   CK(cudaMalloc(&m->drows, nrows * sizeof(double)));
   for (auto& e : m->ev) CK(cudaEventCreate(&e));
+  m->slab_ev.resize((G.ke - G.ks) / 8 + 2);
+  for (auto& e : m->slab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaStreamSynchronize(ctx->stream));
   *out = m;
   return PMHD_OK;
@@ -382,6 +430,7 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   cudaFree(m->drows);
   cudaFreeHost(m->hred);
   for (auto& e : m->ev) if (e) cudaEventDestroy(e);
+  for (auto& e : m->slab_ev) if (e) cudaEventDestroy(e);
   delete m;
   return PMHD_OK;
 }
@@ -523,7 +572,7 @@ int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, 
     if (rc) return rc;
   }
   int n = 0;
-  long long floors = 0;
+  long long floors = 0, fallbacks = 0;
   while ((ncycles < 0 || n < ncycles) && (!(tlim > 0.0) || *t < tlim)) {
     double h = *dt;
     bool last = false;
@@ -532,13 +581,18 @@ int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, 
     double dn = 0.0;
     rc = pmhd_gpu_vl2_step(m, h, &dn, &s);
     floors += s.floor_count;
+    fallbacks += s.fallback_count;
     if (rc) { if (st) *st = s; break; }
     *t = last ? tlim : *t + h;
     *dt = dn;
     ++n;
   }
   if (cycles_done) *cycles_done = n;
-  if (st && rc == PMHD_OK) { st->code = PMHD_OK; st->floor_count = floors; }
+  if (st && rc == PMHD_OK) {
+    st->code = PMHD_OK;
+    st->floor_count = floors;
+    st->fallback_count = fallbacks;
+  }
   return rc;
 }
 

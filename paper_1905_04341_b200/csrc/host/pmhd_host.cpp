@@ -446,7 +446,10 @@ int pmhd_host_config_parse(const char* text, pmhd_run_config* c, int* err_line, 
     else if (key == "dfloor") D(&m.dfloor);
     else if (key == "pfloor") D(&m.pfloor);
     else if (key == "riemann") {
-      if (val == "hlld") m.riemann = PMHD_RIEMANN_HLLD; else if (val == "hlle") m.riemann = PMHD_RIEMANN_HLLE; else ok = false;
+      if (val == "hlld") m.riemann = PMHD_RIEMANN_HLLD;
+      else if (val == "hlle") m.riemann = PMHD_RIEMANN_HLLE;
+      else if (val == "roe") m.riemann = PMHD_RIEMANN_ROE;
+      else ok = false;
     } else if (key == "limiter") {
       if (val == "mc") m.limiter = PMHD_LIMITER_MC; else if (val == "vanleer") m.limiter = PMHD_LIMITER_VANLEER; else ok = false;
     } else if (key == "eos_mode") {

@@ -27,7 +27,7 @@ PMHD_ERR_UNPHYSICAL = 4
 PMHD_ERR_CUDA = 5
 PMHD_ERR_UNSUPPORTED = 6
 
-RIEMANN = {"hlld": 0, "hlle": 1}
+RIEMANN = {"hlld": 0, "hlle": 1, "roe": 2}
 LIMITER = {"mc": 0, "vanleer": 1}
 EOS = {"error": 0, "floor": 1}
 EMF = {"upwind": 0, "arith": 1}
@@ -63,6 +63,7 @@ class Status(C.Structure):
         ("j", C.c_int),
         ("i", C.c_int),
         ("floor_count", C.c_longlong),
+        ("fallback_count", C.c_longlong),
     ]
 
 

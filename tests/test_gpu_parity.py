@@ -31,6 +31,10 @@ CASES = {
                                   wave_n2=1, wave_n3=1, wave_amp=1e-2, riemann="hlle",
                                   limiter="vanleer", emf="arith"), 4),
     "turb3d": (dict(nx1=24, nx2=24, nx3=24, mb1=12, mb2=24, mb3=12, pgen="turbulence"), 4),
+    "wave3d_roe": (dict(nx1=32, nx2=16, nx3=16, mb1=16, mb2=16, mb3=16, x2max=0.5, x3max=0.5,
+                        wave_n1=1, wave_n2=1, wave_amp=1e-3, riemann="roe"), 4),
+    "ot2d_roe": (dict(nx1=64, nx2=64, nx3=1, mb1=32, mb2=64, mb3=1, pgen="orszag_tang", cfl=0.4,
+                      riemann="roe"), 20),
 }
 
 
@@ -203,6 +207,30 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
     o, g, _, _, _ = run_pair(cfg, 3, parity=True)
     for gid in range(cfg.nblocks):
         assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
+
+
+@pytest.mark.parametrize("slab", [8, 16])
+@pytest.mark.parametrize("case", ["blast", "wave"])
+def test_kslab_pipeline_bitwise(gpu_available, slab, case, monkeypatch):
+    """The two-stream k-slab pipeline (flux kernels of slab q+1 overlapping
+    the update kernel of slab q) is bit-identical to the oracle."""
+    monkeypatch.setenv("PMHD_SLAB_PLANES", str(slab))
+    if case == "blast":
+        kw = dict(nx1=32, nx2=32, nx3=64, mb1=32, mb2=16, mb3=32, x1min=-0.5, x1max=0.5,
+                  x2min=-0.5, x2max=0.5, x3min=-1.0, x3max=1.0, pgen="blast", eos_mode="floor",
+                  blast_r=0.2)
+    else:
+        kw = dict(nx1=16, nx2=16, nx3=48, mb1=16, mb2=16, mb3=48, x3max=3.0, wave_n1=1, wave_n3=1,
+                  wave_amp=1e-3)
+    cfg = RunConfig(**kw)
+    o, g, _, (fo, fg), dts = run_pair(cfg, 3, parity=True)
+    assert fo == fg
+    for a, b in dts:
+        assert a == b
+    for gid in range(cfg.nblocks):
+        bo, bg = o.get_block(gid), g.get_block(gid)
+        for f in ("u", "b1f", "b2f", "b3f"):
+            assert np.array_equal(getattr(bo, f), getattr(bg, f)), (gid, f)
 
 
 @pytest.mark.parametrize("nranks", [2, 4])
