@@ -96,6 +96,19 @@ int pmhd_host_wave_eigen(const pmhd_run_config* cfg, double* lambda, double r[7]
 /* Default end time of the problem (one wave period for linear waves). */
 double pmhd_host_default_tlim(const pmhd_run_config* cfg);
 
+/* PMHD1 snapshot: ASCII header lines "PMHD1", "dims n1 n2 n3",
+ * "gamma g", "time t", "END", then little-endian fp64: the 8 conserved
+ * variables over the GLOBAL active grid (variable-major, k-j-i), then the
+ * global staggered b1f, b2f, b3f.  u/b*f[g] are the host arrays of block g
+ * (layout of pmhd_gpu.h).  write: all blocks; read: fills the active cells
+ * and faces of every block (ghosts untouched; exchange afterwards) and checks
+ * dims / gamma -> PMHD_ERR_INPUT on mismatch or a malformed file. */
+int pmhd_host_snapshot_write(const char* path, const pmhd_run_config* cfg, double t,
+                             double* const* u, double* const* b1f, double* const* b2f,
+                             double* const* b3f);
+int pmhd_host_snapshot_read(const char* path, const pmhd_run_config* cfg, double* t, double* const* u,
+                            double* const* b1f, double* const* b2f, double* const* b3f);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2,7 +2,8 @@
 // SPEC.md:445-513) for the GPU path: C++ host code over the two C ABIs
 // (pmhd_host.h: input files + problem generators; pmhd_gpu.h: the solver).
 //
-//   pmhd run   --config <file> [--out <dir>] [--device <d>]   (cmd_run)
+//   pmhd run   --config <file> [--out <dir>] [--device <d>] [--restart <snapshot>]
+//                                                             (cmd_run)
 //   pmhd bench --config <file> [--cycles <n>] [--warmup <w>]  (cmd_bench)
 //
 // run: evolves to tlim (default: one wave period) or nlim cycles, prints
@@ -27,14 +28,14 @@
 namespace {
 
 struct Args {
-  std::string cmd, config, out = ".";
+  std::string cmd, config, out = ".", restart;
   int device = 0, cycles = 10, warmup = 2;
 };
 
 int usage() {
   std::fprintf(stderr,
                "usage: pmhd run|bench --config <file> [--out <dir>] [--device <d>] [--cycles <n>] "
-               "[--warmup <w>]\n");
+               "[--warmup <w>] [--restart <snapshot>]\n");
   return 2;
 }
 
@@ -62,46 +63,6 @@ struct Blocks {
   }
 };
 
-// PMHD1 snapshot: ASCII header, then the 8 conserved variables
-// over the global active grid (variable-major, k-j-i) and the global
-// staggered face arrays, little-endian fp64.
-void write_snapshot(const std::string& path, const pmhd_run_config& cfg, const Blocks& B, double t) {
-  const pmhd_mesh_desc& m = cfg.mesh;
-  const int dim3 = m.nx[2] > 1;
-  const int ng = m.ng, g3 = dim3 ? ng : 0;
-  std::ofstream f(path, std::ios::binary);
-  char hdr[256];
-  std::snprintf(hdr, sizeof(hdr), "PMHD1\ndims %d %d %d\ngamma %.17g\ntime %.17g\nEND\n", m.nx[0],
-                m.nx[1], m.nx[2], m.gamma, t);
-  f << hdr;
-  const int nb0 = m.nx[0] / m.mb[0], nb1 = m.nx[1] / m.mb[1];
-  auto put = [&](double v) { f.write(reinterpret_cast<const char*>(&v), sizeof(v)); };
-  // fn(gid, local k, j, i) over the global grid with extra face layer e[a]
-  auto emit = [&](int ex, int ey, int ez, auto&& get) {
-    for (int k = 0; k < m.nx[2] + ez; ++k)
-      for (int j = 0; j < m.nx[1] + ey; ++j)
-        for (int i = 0; i < m.nx[0] + ex; ++i) {
-          const int ci = std::min(i / m.mb[0], nb0 - 1), cj = std::min(j / m.mb[1], nb1 - 1);
-          const int ck = std::min(k / m.mb[2], m.nx[2] / m.mb[2] - 1);
-          const int gid = (ck * nb1 + cj) * nb0 + ci;
-          put(get(gid, k - ck * m.mb[2] + g3, j - cj * m.mb[1] + ng, i - ci * m.mb[0] + ng));
-        }
-  };
-  for (int v = 0; v < 8; ++v)
-    emit(0, 0, 0, [&](int g, int k, int j, int i) {
-      return B.u[g][v * B.nc + (size_t(k) * B.n[1] + j) * B.n[0] + i];
-    });
-  emit(1, 0, 0, [&](int g, int k, int j, int i) {
-    return B.b1[g][(size_t(k) * B.n[1] + j) * (B.n[0] + 1) + i];
-  });
-  emit(0, 1, 0, [&](int g, int k, int j, int i) {
-    return B.b2[g][(size_t(k) * (B.n[1] + 1) + j) * B.n[0] + i];
-  });
-  emit(0, 0, dim3, [&](int g, int k, int j, int i) {
-    return B.b3[g][(size_t(k) * B.n[1] + j) * B.n[0] + i];
-  });
-}
-
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -113,6 +74,7 @@ int main(int argc, char** argv) {
     auto next = [&]() { return (i + 1 < argc) ? std::string(argv[++i]) : std::string(); };
     if (s == "--config") a.config = next();
     else if (s == "--out") a.out = next();
+    else if (s == "--restart") a.restart = next();
     else if (s == "--device") a.device = std::atoi(next().c_str());
     else if (s == "--cycles") a.cycles = std::atoi(next().c_str());
     else if (s == "--warmup") a.warmup = std::atoi(next().c_str());
@@ -147,14 +109,24 @@ int main(int argc, char** argv) {
   pmhd_host_block_dims(&cfg, dims);
   Blocks B;
   B.alloc(nb, dims);
+  std::vector<double*> pu(nb), p1(nb), p2(nb), p3(nb);
   for (int g = 0; g < nb; ++g) {
-    pmhd_host_pgen_block(&cfg, g, B.u[g].data(), B.b1[g].data(), B.b2[g].data(), B.b3[g].data());
-    pmhd_gpu_upload_block(mesh, g, B.u[g].data(), B.b1[g].data(), B.b2[g].data(), B.b3[g].data());
+    pu[g] = B.u[g].data(); p1[g] = B.b1[g].data(); p2[g] = B.b2[g].data(); p3[g] = B.b3[g].data();
   }
+  double t = 0.0, dt = 0.0;
+  if (!a.restart.empty()) {  // restart from a PMHD1 snapshot
+    if (pmhd_host_snapshot_read(a.restart.c_str(), &cfg, &t, pu.data(), p1.data(), p2.data(),
+                                p3.data()) != PMHD_OK) {
+      std::fprintf(stderr, "restart: %s is not a PMHD1 snapshot of this mesh\n", a.restart.c_str());
+      return 1;
+    }
+  } else {
+    for (int g = 0; g < nb; ++g) pmhd_host_pgen_block(&cfg, g, pu[g], p1[g], p2[g], p3[g]);
+  }
+  for (int g = 0; g < nb; ++g) pmhd_gpu_upload_block(mesh, g, pu[g], p1[g], p2[g], p3[g]);
   pmhd_gpu_exchange(mesh);
   const long long cells = (long long)cfg.mesh.nx[0] * cfg.mesh.nx[1] * cfg.mesh.nx[2];
   pmhd_status st;
-  double t = 0.0, dt = 0.0;
   int done = 0;
 
   if (a.cmd == "bench") {
@@ -196,7 +168,8 @@ int main(int argc, char** argv) {
     pmhd_gpu_download_block(mesh, g, B.u[g].data(), nullptr, B.b1[g].data(), B.b2[g].data(),
                             B.b3[g].data());
   mkdir(a.out.c_str(), 0755);
-  write_snapshot(a.out + "/snapshot.pmhd", cfg, B, t);
+  pmhd_host_snapshot_write((a.out + "/snapshot.pmhd").c_str(), &cfg, t, pu.data(), p1.data(), p2.data(),
+                           p3.data());
   if (cfg.pgen == PMHD_PGEN_LINEAR_WAVE) {  // l1_error -> errors.csv
     std::vector<double> ex(8 * B.nc);
     double l1[8] = {0};

@@ -133,6 +133,32 @@ class RunConfig:
             raise ConfigError("no eigenmode")
         return lam.value, np.array(list(r)), res.value
 
+    # ---- PMHD1 snapshot / restart -------------------------------
+    @staticmethod
+    def _ptrs(blocks, field):
+        arr = (N._dp * len(blocks))(*[N.dptr(getattr(b, field)) for b in blocks])
+        return arr
+
+    def snapshot_write(self, path, blocks, t):
+        """blocks: one BlockState per gid (all blocks of the mesh)."""
+        rc = N.host_lib().pmhd_host_snapshot_write(
+            str(path).encode(), C.byref(self.c), float(t), *[self._ptrs(blocks, f) for f in
+                                                          ("u", "b1f", "b2f", "b3f")])
+        if rc != N.PMHD_OK:
+            raise OSError(f"snapshot write failed: {path}")
+
+    def snapshot_read(self, path):
+        """Returns (blocks, t): the active cells and faces of every block
+        (ghosts zero; run exchange_ghosts after loading)."""
+        blocks = [self.new_block() for _ in range(self.nblocks)]
+        t = C.c_double()
+        rc = N.host_lib().pmhd_host_snapshot_read(
+            str(path).encode(), C.byref(self.c), C.byref(t), *[self._ptrs(blocks, f) for f in
+                                                             ("u", "b1f", "b2f", "b3f")])
+        if rc != N.PMHD_OK:
+            raise ParseError(0, f"not a PMHD1 snapshot of this mesh: {path}")
+        return blocks, t.value
+
     def default_tlim(self) -> float:
         return N.host_lib().pmhd_host_default_tlim(C.byref(self.c))
 

@@ -138,6 +138,9 @@ def host_lib() -> C.CDLL:
         L.pmhd_host_wave_eigen.argtypes = [_P(RunConfigC), _dp, _dp, _dp]
         L.pmhd_host_default_tlim.argtypes = [_P(RunConfigC)]
         L.pmhd_host_default_tlim.restype = C.c_double
+        _pp = _P(_dp)
+        L.pmhd_host_snapshot_write.argtypes = [C.c_char_p, _P(RunConfigC), C.c_double, _pp, _pp, _pp, _pp]
+        L.pmhd_host_snapshot_read.argtypes = [C.c_char_p, _P(RunConfigC), _dp, _pp, _pp, _pp, _pp]
         _host = L
     return _host
 
