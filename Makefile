@@ -51,5 +51,6 @@ clean:
 # A/B experiment builds (bench.py honours PMHD_GPU_LIB=<path>)
 exp: $(GPU_DEPS)
 	@mkdir -p $(LIB)/exp
-	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_MINB=5 -shared -o $(LIB)/exp/libpmhd_gpu_minb5.so $(GPU_SRCS)
-	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_MINB=3 -shared -o $(LIB)/exp/libpmhd_gpu_minb3.so $(GPU_SRCS)
+	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_SMEMW=0 -DPMHD_FLUX_MINB=4 -shared -o $(LIB)/exp/libpmhd_gpu_regs.so $(GPU_SRCS)
+	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_MINB=4 -shared -o $(LIB)/exp/libpmhd_gpu_minb4.so $(GPU_SRCS)
+	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_MINB=6 -shared -o $(LIB)/exp/libpmhd_gpu_minb6.so $(GPU_SRCS)

@@ -27,9 +27,19 @@ namespace {
 constexpr int FX = 32;  // faces along i per tile
 constexpr int FS = 8;   // faces along the second tile axis
 constexpr int NTHR = 128;
-#ifndef PMHD_FLUX_MINB
-#define PMHD_FLUX_MINB 4
+#ifndef PMHD_FLUX_SMEMW
+#define PMHD_FLUX_SMEMW 1
 #endif
+// Resident CTAs per SM the register budget is sized for: Roe needs ~130
+// registers (4 CTAs); HLLD with shared-memory side states (SmemW) and HLLE
+// fit 96 (5 CTAs, 20 warps; shared memory allows 5 for the 39 KB x2/x3 tiles).
+#ifndef PMHD_FLUX_MINB
+#define PMHD_FLUX_MINB 5
+#endif
+template <int RS>
+struct FluxMinB {
+  static constexpr int value = (RS == PMHD_RIEMANN_ROE) ? 4 : PMHD_FLUX_MINB;
+};
 
 template <int DIR>
 struct TileShape {
@@ -47,8 +57,8 @@ __device__ __forceinline__ int rot_var(int n) {
   return V[DIR][n];
 }
 
-template <int DIR>
-__global__ void __launch_bounds__(NTHR, PMHD_FLUX_MINB)
+template <int DIR, int RS>
+__global__ void __launch_bounds__(NTHR, FluxMinB<RS>::value)
 k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024,
              int stage, DevRed* red, int write_ec, int f_i0, int f_i1, int f_s0, int f_s1, int f_t0,
              int f_t1, int ty0) {
@@ -65,21 +75,50 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   double* const* S = B.st[sel];
 
   // ---- phase 1: load + cons_to_prim of the stencil cells into smem --------
-  for (int c = threadIdx.x; c < TS::NCELL; c += NTHR) {
+  // All PER cells' loads are issued before any is consumed (memory-level
+  // parallelism: up to 3 x 11 loads in flight per thread).
+  double ub[TS::PER][11];
+  long long cid[TS::PER];
+#pragma unroll
+  for (int p = 0; p < TS::PER; ++p) {
+    const int c = threadIdx.x + p * NTHR;
     const int col = c % TS::NCOL, row = c / TS::NCOL;
     int i, j, k;
     if (DIR == 0) { i = fi0 - 2 + col; j = fs0 + row; k = t3; }
     else if (DIR == 1) { i = fi0 + col; j = fs0 - 2 + row; k = t3; }
     else { i = fi0 + col; k = fs0 - 2 + row; j = t3; }
-    if (i < 0 || i >= G.n1 || j < 0 || j >= G.n2 || k < 0 || k >= G.n3) continue;
-    const long long id = G.idx(k, j, i);
+    cid[p] = -1;
+    if (c < TS::NCELL && i >= 0 && i < G.n1 && j >= 0 && j < G.n2 && k >= 0 && k < G.n3) {
+      const long long id = G.idx(k, j, i);
+      cid[p] = id;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) ub[p][v] = __ldg(S[v] + id);
+      ub[p][5] = __ldg(S[5] + id);
+      ub[p][6] = __ldg(S[5] + id + 1);
+      ub[p][7] = __ldg(S[6] + id);
+      ub[p][8] = __ldg(S[6] + id + G.sx);
+      ub[p][9] = __ldg(S[7] + id);
+      ub[p][10] = __ldg(S[7] + id + G.sy);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < TS::PER; ++p) {
+    if (cid[p] < 0) continue;
+    const int c = threadIdx.x + p * NTHR;
+    const long long id = cid[p];
     double u[5], bc[3], w[8];
 #pragma unroll
-    for (int v = 0; v < 5; ++v) u[v] = __ldg(S[v] + id);
-    bc[0] = 0.5 * (__ldg(S[5] + id) + __ldg(S[5] + id + 1));
-    bc[1] = 0.5 * (__ldg(S[6] + id) + __ldg(S[6] + id + G.sx));
-    bc[2] = 0.5 * (__ldg(S[7] + id) + __ldg(S[7] + id + G.sy));
+    for (int v = 0; v < 5; ++v) u[v] = ub[p][v];
+    bc[0] = 0.5 * (ub[p][5] + ub[p][6]);
+    bc[1] = 0.5 * (ub[p][7] + ub[p][8]);
+    bc[2] = 0.5 * (ub[p][9] + ub[p][10]);
     const int fl = cons_to_prim(u, bc, ph, w, false);
+    // (k, j, i) of the cell from its tile position
+    const int col = c % TS::NCOL, row = c / TS::NCOL;
+    int i, j, k;
+    if (DIR == 0) { i = fi0 - 2 + col; j = fs0 + row; k = t3; }
+    else if (DIR == 1) { i = fi0 + col; j = fs0 - 2 + row; k = t3; }
+    else { i = fi0 + col; k = fs0 - 2 + row; j = t3; }
     if ((fl & 4) && k >= G.ks && k < G.ke && j >= G.js && j < G.je && i >= G.is && i < G.ie) {
       const long long gi = (long long)B.c[0] * G.mb[0] + (i - G.is);
       const long long gj = (long long)B.c[1] * G.mb[1] + (j - G.js);
@@ -144,19 +183,27 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     if (fi >= f_i1 || fs >= f_s1) continue;
     const int cl = fr * TS::NCOL + fc + TS::DC;  // cell on the low side of the face
     const int ch = cl + TS::DC;                  // cell on the high side
-    double wl[7], wr[7];
-#pragma unroll
-    for (int n = 0; n < 7; ++n) {
-      wl[n] = wsrc[n * TS::NCELL + cl];
-      wr[n] = sw[n][ch];
-    }
     int i, j, k;
     if (DIR == 0) { i = fi; j = fs; k = t3; }
     else if (DIR == 1) { i = fi; j = fs; k = t3; }
     else { i = fi; k = fs; j = t3; }
     const long long id = G.idx(k, j, i);
+    const double bn = __ldg(S[5 + DIR] + id);
     double out[8];
-    if (face_solve(wl, wr, __ldg(S[5 + DIR] + id), ph, c1024, out))
+    int fb;
+    if constexpr (PMHD_FLUX_SMEMW && RS == PMHD_RIEMANN_HLLD) {
+      const SmemW wl{wsrc + cl, TS::NCELL}, wr{&sw[0][0] + ch, TS::NCELL};
+      fb = face_solve<RS>(wl, wr, bn, ph, c1024, out);
+    } else {
+      double wl[7], wr[7];
+#pragma unroll
+      for (int n = 0; n < 7; ++n) {
+        wl[n] = wsrc[n * TS::NCELL + cl];
+        wr[n] = sw[n][ch];
+      }
+      fb = face_solve<RS>(wl, wr, bn, ph, c1024, out);
+    }
+    if (fb)
       atomicAdd(&red[stage].fallback_count, 1ULL);
     double* const* F = B.fx[DIR];
     F[0][id] = out[0];
@@ -202,15 +249,20 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
     }
   }
   const dim3 grid((i1 - i0 + FX - 1) / FX, ty1 - ty0, (nt1 - nt0) * G.nb);
-  if (dir == 0)
-    k_flux_fused<0><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, i1,
-                                          ns0, ns1, nt0, nt1, ty0);
-  else if (dir == 1)
-    k_flux_fused<1><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, i1,
-                                          ns0, ns1, nt0, nt1, ty0);
-  else
-    k_flux_fused<2><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, i1,
-                                          ns0, ns1, nt0, nt1, ty0);
+#define PMHD_FLUX_LAUNCH(D, R)                                                                    \
+  k_flux_fused<D, R><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, \
+                                           i1, ns0, ns1, nt0, nt1, ty0)
+#define PMHD_FLUX_DIRS(R)                          \
+  do {                                             \
+    if (dir == 0) PMHD_FLUX_LAUNCH(0, R);          \
+    else if (dir == 1) PMHD_FLUX_LAUNCH(1, R);     \
+    else PMHD_FLUX_LAUNCH(2, R);                   \
+  } while (0)
+  if (ph.riemann == PMHD_RIEMANN_HLLE) PMHD_FLUX_DIRS(PMHD_RIEMANN_HLLE);
+  else if (ph.riemann == PMHD_RIEMANN_ROE) PMHD_FLUX_DIRS(PMHD_RIEMANN_ROE);
+  else PMHD_FLUX_DIRS(PMHD_RIEMANN_HLLD);
+#undef PMHD_FLUX_DIRS
+#undef PMHD_FLUX_LAUNCH
 }
 
 }  // namespace pmhd_gpu

@@ -54,7 +54,7 @@ struct pmhd_mesh {
   bool all_local = true;
   bool prof = false;
   int variant = 0;                // 0: fused flux kernels; 1: split (debug; PMHD_KERNELS=split)
-  int slab_planes = 64;           // k-slab pipeline depth (PMHD_SLAB_PLANES, 0 = off)
+  int slab_planes = 0;            // k-slab pipeline depth (PMHD_SLAB_PLANES, 0 = off)
   std::vector<cudaEvent_t> slab_ev;
   cudaEvent_t ev[8] = {};
   pmhd_region_times times{};

@@ -10,6 +10,10 @@ want = {
   "fp64_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
   "ipc": "sm__inst_executed.avg.per_cycle_active", "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
   "smem_B": "launch__shared_mem_per_block_static",
+  "dfma": "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+  "dmul": "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+  "dadd": "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+  "inst": "smsp__inst_executed.sum",
 }
 stalls = [k for k in h if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")]
 for row in r:
