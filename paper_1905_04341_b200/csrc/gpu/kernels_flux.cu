@@ -144,17 +144,25 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   // ---- phase 2: per-cell reconstruction, one variable at a time ------------
   if (plm) {
     constexpr int LEN = (DIR == 0) ? TS::NCOL : TS::NROW;
+    // which of this thread's cells have both stencil neighbours in the tile
+    // (evaluated once, not per variable)
+    unsigned vmask = 0;
+#pragma unroll
+    for (int p = 0; p < TS::PER; ++p) {
+      const int c = threadIdx.x + p * NTHR;
+      const int pos = (DIR == 0) ? c % TS::NCOL : c / TS::NCOL;
+      if (c < TS::NCELL && pos >= 1 && pos <= LEN - 2) vmask |= 1u << p;
+    }
 #pragma unroll 1
     for (int n = 0; n < 7; ++n) {
       double lo[TS::PER], hi[TS::PER];
+      double* const q = &sw[n][threadIdx.x];
 #pragma unroll
       for (int p = 0; p < TS::PER; ++p) {
-        const int c = threadIdx.x + p * NTHR;
-        const int pos = (DIR == 0) ? c % TS::NCOL : c / TS::NCOL;
         lo[p] = hi[p] = 0.0;
-        if (c < TS::NCELL && pos >= 1 && pos <= LEN - 2) {
-          const double q0 = sw[n][c];
-          const double dq = plm_slope(sw[n][c - TS::DC], q0, sw[n][c + TS::DC], ph.limiter);
+        if (vmask & (1u << p)) {
+          const double q0 = q[p * NTHR];
+          const double dq = plm_slope(q[p * NTHR - TS::DC], q0, q[p * NTHR + TS::DC], ph.limiter);
           hi[p] = q0 + 0.5 * dq;  // wL of the face above (oracle: qm1 + 0.5*slope)
           lo[p] = q0 - 0.5 * dq;  // wR of the face below (oracle: q0 - 0.5*slope)
         }
@@ -162,11 +170,9 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       __syncthreads();  // all reads of sw[n] done before it is overwritten
 #pragma unroll
       for (int p = 0; p < TS::PER; ++p) {
-        const int c = threadIdx.x + p * NTHR;
-        const int pos = (DIR == 0) ? c % TS::NCOL : c / TS::NCOL;
-        if (c < TS::NCELL && pos >= 1 && pos <= LEN - 2) {
-          sw[n][c] = lo[p];
-          sp[n][c] = hi[p];
+        if (vmask & (1u << p)) {
+          q[p * NTHR] = lo[p];
+          sp[n][threadIdx.x + p * NTHR] = hi[p];
         }
       }
     }
