@@ -19,12 +19,12 @@ constexpr int kNState = 8;  // u0..u4 (rho, m1, m2, m3, E), b1f, b2f, b3f
 
 struct KGeom {
   int n1, n2, n3;     // cell extents incl. ghosts
-  long long sx, sy;   // row / plane pitch (doubles)
+  int sx, sy;         // row / plane pitch (doubles; a block array is < 2^31 doubles)
   int is, ie, js, je, ks, ke;
   int dim, nb, ng;
   int nx[3], mb[3];
   double dx[3];
-  __host__ __device__ long long idx(int k, int j, int i) const { return k * sy + j * sx + i; }
+  __host__ __device__ int idx(int k, int j, int i) const { return k * sy + j * sx + i; }
 };
 
 struct DevBlock {

@@ -78,7 +78,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   // All PER cells' loads are issued before any is consumed (memory-level
   // parallelism: up to 3 x 11 loads in flight per thread).
   double ub[TS::PER][11];
-  long long cid[TS::PER];
+  int cid[TS::PER];
 #pragma unroll
   for (int p = 0; p < TS::PER; ++p) {
     const int c = threadIdx.x + p * NTHR;
@@ -89,7 +89,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     else { i = fi0 + col; k = fs0 - 2 + row; j = t3; }
     cid[p] = -1;
     if (c < TS::NCELL && i >= 0 && i < G.n1 && j >= 0 && j < G.n2 && k >= 0 && k < G.n3) {
-      const long long id = G.idx(k, j, i);
+      const int id = G.idx(k, j, i);
       cid[p] = id;
 #pragma unroll
       for (int v = 0; v < 5; ++v) ub[p][v] = __ldg(S[v] + id);
@@ -105,7 +105,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   for (int p = 0; p < TS::PER; ++p) {
     if (cid[p] < 0) continue;
     const int c = threadIdx.x + p * NTHR;
-    const long long id = cid[p];
+    const int id = cid[p];
     double u[5], bc[3], w[8];
 #pragma unroll
     for (int v = 0; v < 5; ++v) u[v] = ub[p][v];
@@ -193,7 +193,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     if (DIR == 0) { i = fi; j = fs; k = t3; }
     else if (DIR == 1) { i = fi; j = fs; k = t3; }
     else { i = fi; k = fs; j = t3; }
-    const long long id = G.idx(k, j, i);
+    const int id = G.idx(k, j, i);
     const double bn = __ldg(S[5 + DIR] + id);
     double out[8];
     int fb;

@@ -22,7 +22,7 @@ __global__ void k_halo_copy(double* const* arrays, KGeom G, HaloSlab sl, double*
   const int i = sl.org[v][0] + (int)(l % ni);
   const int j = sl.org[v][1] + (int)((l / ni) % nj);
   const int k = sl.org[v][2] + (int)(l / ((long long)ni * nj));
-  const long long id = G.idx(k, j, i);
+  const int id = G.idx(k, j, i);
   if (to_buf) buf[t] = arrays[v][id];
   else arrays[v][id] = buf[t];
 }

@@ -88,7 +88,7 @@ __device__ __forceinline__ double dt_cell(const KGeom& G, const KPhys& ph, const
   return t;
 }
 
-__device__ __forceinline__ void load_bcc(double* const* S, const KGeom& G, long long id, double* bc) {
+__device__ __forceinline__ void load_bcc(double* const* S, const KGeom& G, int id, double* bc) {
   bc[0] = 0.5 * (S[5][id] + S[5][id + 1]);
   bc[1] = 0.5 * (S[6][id] + S[6][id + G.sx]);
   bc[2] = 0.5 * (S[7][id] + S[7][id + G.sy]);
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(TX* TY) k_c2p_all(const DevBlock* __restrict__
   BOX_INDEX(bx);
   const DevBlock& B = blks[b];
   double* const* S = B.st[sel];
-  const long long id = G.idx(k, j, i);
+  const int id = G.idx(k, j, i);
   double u[5], bc[3], w[8];
 #pragma unroll
   for (int v = 0; v < 5; ++v) u[v] = S[v][id];
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(TX* TY) k_flux(const DevBlock* __restrict__ bl
                                                  int sel, int plm, double c1024, Box bx) {
   BOX_INDEX(bx);
   const DevBlock& B = blks[b];
-  const long long off = (DIR == 0) ? 1 : ((DIR == 1) ? G.sx : G.sy);
+  const int off = (DIR == 0) ? 1 : ((DIR == 1) ? G.sx : G.sy);
   // rotated variable map: (d, vn, vt1, vt2, p, bt1, bt2)
   constexpr int V0 = 0, V4 = 4;
   constexpr int V1 = (DIR == 0) ? 1 : ((DIR == 1) ? 2 : 3);
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(TX* TY) k_flux(const DevBlock* __restrict__ bl
   constexpr int V5 = (DIR == 0) ? 6 : ((DIR == 1) ? 7 : 5);
   constexpr int V6 = (DIR == 0) ? 7 : ((DIR == 1) ? 5 : 6);
   const int vars[7] = {V0, V1, V2, V3, V4, V5, V6};
-  const long long id = G.idx(k, j, i);
+  const int id = G.idx(k, j, i);
   double wl[7], wr[7];
 #pragma unroll
   for (int n = 0; n < 7; ++n) {
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(TX* TY) k_flux(const DevBlock* __restrict__ bl
   F[7][id] = out[7];
 }
 
-__device__ __forceinline__ double ecc(const DevBlock& B, int comp, long long id) {
+__device__ __forceinline__ double ecc(const DevBlock& B, int comp, int id) {
   const double v1 = B.w[1][id], v2 = B.w[2][id], v3 = B.w[3][id];
   const double b1 = B.w[5][id], b2 = B.w[6][id], b3 = B.w[7][id];
   if (comp == 0) return v3 * b2 - v2 * b3;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(TX* TY) k_emf(const DevBlock* __restrict__ blk
                                                 Box bx) {
   BOX_INDEX(bx);
   const DevBlock& B = blks[b];
-  const long long id = G.idx(k, j, i), sx = G.sx, sy = G.sy;
+  const int id = G.idx(k, j, i), sx = G.sx, sy = G.sy;
   double* const* X1 = B.fx[0];
   double* const* X2 = B.fx[1];
   double* const* X3 = B.fx[2];
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(TX* TY) k_update(const DevBlock* __restrict__ 
                                                    KStage ks, Box bx) {
   BOX_INDEX(bx);
   const DevBlock& B = blks[b];
-  const long long id = G.idx(k, j, i), sx = G.sx, sy = G.sy;
+  const int id = G.idx(k, j, i), sx = G.sx, sy = G.sy;
   double* const* base = B.st[0];
   double* const* out = B.st[ks.out_sel];
   const bool d3 = (G.dim == 3);
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(TX* TY) k_c2p_end(const DevBlock* __restrict__
   if (i < bx.i1 && j < bx.j1) {
     const DevBlock& B = blks[b];
     double* const* S = B.st[ks.out_sel];
-    const long long id = G.idx(k, j, i);
+    const int id = G.idx(k, j, i);
     double u[5], bc[3], w[8];
 #pragma unroll
     for (int v = 0; v < 5; ++v) u[v] = S[v][id];
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(TX* TY) k_dt_state(const DevBlock* __restrict_
   if (i < bx.i1 && j < bx.j1) {
     const DevBlock& B = blks[b];
     double* const* S = B.st[0];
-    const long long id = G.idx(k, j, i);
+    const int id = G.idx(k, j, i);
     double u[5], bc[3], w[8];
 #pragma unroll
     for (int v = 0; v < 5; ++v) u[v] = S[v][id];
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(TX* TY) k_divb(const DevBlock* __restrict__ bl
   double m = 0.0;
   if (i < bx.i1 && j < bx.j1) {
     double* const* S = blks[b].st[0];
-    const long long id = G.idx(k, j, i);
+    const int id = G.idx(k, j, i);
     const double d = (S[5][id + 1] - S[5][id]) / G.dx[0] + (S[6][id + G.sx] - S[6][id]) / G.dx[1] +
                      (S[7][id + G.sy] - S[7][id]) / G.dx[2];
     m = fabs(d);

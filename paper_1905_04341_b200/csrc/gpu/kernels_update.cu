@@ -46,7 +46,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   double* const* X1 = B.fx[0];
   double* const* X2 = B.fx[1];
   double* const* X3 = B.fx[2];
-  const long long sx = G.sx, sy = G.sy;
+  const int sx = G.sx, sy = G.sy;
   const int tid = threadIdx.x;
 
   // ---- P1: cell-centred E of the stage-input state ------------------------
@@ -58,7 +58,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
     const int ii = i0 - 1 + c, jj = j0 - 1 + r, kk = d3 ? k - 1 + pl : k;
     const int ps = d3 ? pl : 1;
     if (c > nx + 1 || r > ny + 1) continue;
-    const long long id = G.idx(kk, jj, ii);
+    const int id = G.idx(kk, jj, ii);
     // written by the last-direction flux kernel from the same primitives
     ec[0][ps][r][c] = __ldg(B.ec[0] + id);
     ec[1][ps][r][c] = __ldg(B.ec[1] + id);
@@ -72,7 +72,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   for (int q = tid; q < (UY + 1) * (UX + 1); q += UTHR) {  // E3 at plane k
     const int c = q % (UX + 1), r = q / (UX + 1);
     if (c > nx || r > ny) continue;
-    const long long id = G.idx(k, j0 + r, i0 + c);
+    const int id = G.idx(k, j0 + r, i0 + c);
     const int ec_c = c + 1, ec_r = r + 1;
     e3s[r][c] = corner_emf(mode, X1[5][id], X1[5][id - sx], X2[6][id], X2[6][id - 1], X1[7][id],
                            X1[7][id - sx], X2[7][id], X2[7][id - 1], ec[2][1][ec_r][ec_c],
@@ -84,7 +84,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
     const int c = q % UX, r = (q / UX) % (UY + 1), h = q / (UX * (UY + 1));
     if (c >= nx || r > ny) continue;
     const int kk = k + h;
-    const long long id = G.idx(d3 ? kk : k, j0 + r, i0 + c);
+    const int id = G.idx(d3 ? kk : k, j0 + r, i0 + c);
     double e;
     if (d3) {
       const int pa = 1 + h, pm = h;  // Ec planes of kk and kk-1
@@ -101,7 +101,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
     const int c = q % (UX + 1), r = (q / (UX + 1)) % UY, h = q / ((UX + 1) * UY);
     if (c > nx || r >= ny) continue;
     const int kk = k + h;
-    const long long id = G.idx(d3 ? kk : k, j0 + r, i0 + c);
+    const int id = G.idx(d3 ? kk : k, j0 + r, i0 + c);
     double e;
     if (d3) {
       const int pa = 1 + h, pm = h;
@@ -120,7 +120,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   for (int q = tid; q < UY * (UX + 1); q += UTHR) {  // b1f, faces i0 .. i0+nx
     const int c = q % (UX + 1), r = q / (UX + 1);
     if (c > nx || r >= ny) continue;
-    const long long id = G.idx(k, j0 + r, i0 + c);
+    const int id = G.idx(k, j0 + r, i0 + c);
     double v;
     if (d3) v = Sb[5][id] - (c2 * (e3s[r + 1][c] - e3s[r][c]) - c3 * (e2s[1][r][c] - e2s[0][r][c]));
     else v = Sb[5][id] - c2 * (e3s[r + 1][c] - e3s[r][c]);
@@ -130,7 +130,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   for (int q = tid; q < (UY + 1) * UX; q += UTHR) {  // b2f, faces j0 .. j0+ny
     const int c = q % UX, r = q / UX;
     if (c >= nx || r > ny) continue;
-    const long long id = G.idx(k, j0 + r, i0 + c);
+    const int id = G.idx(k, j0 + r, i0 + c);
     double v;
     if (d3) v = Sb[6][id] - (c3 * (e1s[1][r][c] - e1s[0][r][c]) - c1 * (e3s[r][c + 1] - e3s[r][c]));
     else v = Sb[6][id] + c1 * (e3s[r][c + 1] - e3s[r][c]);
@@ -140,7 +140,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   for (int q = tid; q < 2 * UY * UX; q += UTHR) {  // b3f, faces k and k+1
     const int c = q % UX, r = (q / UX) % UY, h = q / (UX * UY);
     if (c >= nx || r >= ny) continue;
-    const long long id = G.idx(k + h, j0 + r, i0 + c);
+    const int id = G.idx(k + h, j0 + r, i0 + c);
     const double v = Sb[7][id] - (c1 * (e2s[h][r][c + 1] - e2s[h][r][c]) -
                                   c2 * (e1s[h][r + 1][c] - e1s[h][r][c]));
     b3s[h][r][c] = v;
@@ -154,7 +154,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
     const int c = tid % UX, r = tid / UX;
     if (c < nx && r < ny) {
       const int i = i0 + c, j = j0 + r;
-      const long long id = G.idx(k, j, i);
+      const int id = G.idx(k, j, i);
       double u[5];
 #pragma unroll
       for (int v = 0; v < 5; ++v) {

@@ -333,8 +333,16 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   G.n1 = G.mb[0] + 2 * G.ng;
   G.n2 = G.mb[1] + 2 * G.ng;
   G.n3 = (G.dim == 3) ? G.mb[2] + 2 * G.ng : 1;
-  G.sx = ((G.n1 + 1 + 31) / 32) * 32;
-  G.sy = G.sx * (G.n2 + 1);
+  {
+    // kernels index a block array with 32-bit ints (idx(k,j,i) = k*sy + j*sx + i)
+    const long long sx = ((G.n1 + 1 + 31) / 32) * 32, sy = sx * (G.n2 + 1);
+    if ((long long)(G.n3 + 1) * sy + 64 >= (1LL << 31)) {
+      delete m;
+      return fail(ctx, PMHD_ERR_CONFIG, "MeshBlock too large (a block array must hold < 2^31 doubles): use smaller blocks");
+    }
+    G.sx = int(sx);
+    G.sy = int(sy);
+  }
   G.is = G.ng; G.ie = G.ng + G.mb[0];
   G.js = G.ng; G.je = G.ng + G.mb[1];
   if (G.dim == 3) { G.ks = G.ng; G.ke = G.ng + G.mb[2]; } else { G.ks = 0; G.ke = 1; }
