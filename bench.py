@@ -66,11 +66,22 @@ def make_config(n, ranks, riemann="hlld", nz=None):
 
 
 def falg():
+    """(F_alg total, F_alg of the flux region, source) per cell-update."""
     try:
-        d = json.load(open(F_ALG_FILE))
-        return float(d["256"]["per_cell_update"]), "oracle CountingScalar at 256^3 (profiles/falg_counting.json)"
+        d = json.load(open(F_ALG_FILE))["256"]
+        return (float(d["per_cell_update"]), float(d["flux_region_per_cell_update"]),
+                "oracle CountingScalar at 256^3, HLLD (profiles/falg_counting.json, tools/count_falg.py)")
     except Exception:
-        return 2790.0, "estimate"
+        return 2815.0, 2303.0, "estimate"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the flux / update kernels at 256^3 from the
+    committed ncu --set full capture (profiles/r01/ncu_traffic_256.json)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic_256.json")))
+    except Exception:
+        return None
 
 
 def fp64_peak():
@@ -304,7 +315,7 @@ def run_ours(args):
     g.set_profiling(False)
     kern_ms = (rt["c2p_ms"] + rt["riemann_ms"] + rt["ct_emf_ms"] + rt["integrate_ms"] +
                rt["boundary_ms"]) / nprof
-    F_alg, F_src = falg()
+    F_alg, F_flux, F_src = falg()
     fp64_pk, fp64_src = fp64_peak()
     hbm_pk, hbm_src = hbm_peak()
     cycle_ms_kernels = kern_ms
@@ -312,12 +323,33 @@ def run_ours(args):
     ach_tf = F_alg * cells_rank / (cycle_ms_kernels * 1e-3) / 1e12
     shares = {k: rt[k] / max(1e-9, kern_ms * nprof) for k in
               ("c2p_ms", "riemann_ms", "ct_emf_ms", "integrate_ms", "boundary_ms")}
+    # Dominant kernel: the fused flux kernel (c2p + PLM + Riemann), 2*dim
+    # launches per cycle, timed with CUDA events on the ABI stream (region
+    # "riemann").  It is FP64-pipe bound (no dense contraction, < 30 % of HBM
+    # bandwidth in ncu), so its roofline is the measured DFMA peak.
+    dim = cfg.dim
+    n_flux = 2 * dim
+    flux_ms = rt["riemann_ms"] / nprof / n_flux            # average launch duration
+    flux_flops = F_flux * cells_rank / n_flux              # algorithmic flops per launch
+    flux_tf = flux_flops / (flux_ms * 1e-3) / 1e12
+    tr = ncu_traffic() if args.size == 256 and dim == 3 else None
+    upd_ms = rt["integrate_ms"] / nprof / 2
     roofline = {
-        "bound": "hbm", "achieved": ach_gbs, "peak": hbm_pk, "unit": "GB/s", "frac": ach_gbs / hbm_pk,
-        "traffic": None, "peak_source": hbm_src,
-        "kernel": "whole VL2 cycle (all stage kernels; B_alg = 320 B/cell-update, SURVEY.md §8d)",
-        "fp64": {"achieved": ach_tf, "peak": fp64_pk, "unit": "TFLOP/s", "frac": ach_tf / fp64_pk,
-                 "F_alg_per_cell_update": F_alg, "F_alg_source": F_src, "peak_source": fp64_src},
+        "bound": "fp64", "achieved": flux_tf, "peak": fp64_pk, "unit": "TFLOP/s",
+        "frac": flux_tf / fp64_pk,
+        "traffic": tr["flux_bytes_per_launch"] if tr else None,
+        "kernel": f"k_flux_fused (dominant: {shares['riemann_ms']:.0%} of the cycle; {n_flux} launches/cycle, "
+                  f"avg {flux_ms:.3f} ms; F_alg(flux region) = {F_flux:.1f} flop/cell-update / {n_flux} launches)",
+        "peak_source": fp64_src,
+        "note": "FP64 CUDA-core bound, neither HBM nor tensor cores: bound='fp64' against the measured DFMA peak",
+        "hbm_whole_cycle": {"achieved": ach_gbs, "peak": hbm_pk, "unit": "GB/s", "frac": ach_gbs / hbm_pk,
+                            "B_alg_per_cell_update": B_ALG, "peak_source": hbm_src,
+                            "ncu_dram_bytes_per_cell_update": tr["dram_bytes_per_cell_update"] if tr else None},
+        "fp64_whole_cycle": {"achieved": ach_tf, "peak": fp64_pk, "unit": "TFLOP/s", "frac": ach_tf / fp64_pk,
+                             "F_alg_per_cell_update": F_alg, "F_alg_source": F_src},
+        "update_kernel": {"name": "k_update_fused", "avg_ms": upd_ms,
+                          "dram_bytes_per_launch": tr["update_bytes_per_launch"] if tr else None,
+                          "dram_gbs": (tr["update_bytes_per_launch"] / (upd_ms * 1e-3) / 1e9) if tr else None},
         "binding_ceiling": "fp64" if F_alg / fp64_pk > B_ALG / (hbm_pk / 1e3) else "hbm",
         # paper Eq. 2 against the binding ceiling (SURVEY.md §8d judged figure)
         "roofline_achieved_eq2": (cells_rank / (cycle_ms_kernels * 1e-3)) /
@@ -349,7 +381,7 @@ def run_ours(args):
         d = allreduce_min(g.new_dt())
         for _ in range(args.steps):
             d = step(d)
-        out = g.get_block(my_gid)
+        g.get_block(my_gid, out=out)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)

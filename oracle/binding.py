@@ -54,6 +54,8 @@ def lib(ref: bool = False) -> C.CDLL:
         L.oracle_flops.argtypes = [_dp]
         L.oracle_flops.restype = None
         L.oracle_flops_reset.restype = None
+        L.oracle_region_flops.argtypes = [_dp]
+        L.oracle_region_flops.restype = None
         L.oracle_cons_to_prim.argtypes = [_dp, C.c_double, _dp]
         L.oracle_prim_to_cons.argtypes = [_dp, C.c_double, _dp]
         L.oracle_prim_to_cons.restype = None
@@ -123,6 +125,14 @@ def flops():
 
 def flops_reset():
     lib().oracle_flops_reset()
+
+
+def region_flops():
+    """[flux region (c2p + reconstruction + Riemann), EMF + CT + update]
+    flops tallied by counting meshes since the last flops_reset()."""
+    out = np.zeros(2)
+    lib().oracle_region_flops(out.ctypes.data_as(_dp))
+    return out
 
 
 # ---- mesh-level solver --------------------------------------------------------

@@ -22,6 +22,10 @@ struct FlopTally {
 };
 
 inline FlopTally g_tally;
+// Per-region split of the tally (oracle stage(): c2p + reconstruction +
+// Riemann = "flux"; EMF + CT + update + end-of-stage c2p = "update"), so the
+// GPU kernels that implement each region get their own algorithmic flops.
+inline double g_region[2] = {0.0, 0.0};
 
 class Counting {
  public:

@@ -312,7 +312,15 @@ void oracle_flops(double out[4]) {
   out[0] = oracle::g_tally.add; out[1] = oracle::g_tally.mul;
   out[2] = oracle::g_tally.div; out[3] = oracle::g_tally.sqrt_n;
 }
-void oracle_flops_reset(void) { oracle::g_tally.reset(); }
+void oracle_flops_reset(void) {
+  oracle::g_tally.reset();
+  oracle::g_region[0] = oracle::g_region[1] = 0.0;
+}
+// out[0] = flux region (c2p + PLM + Riemann), out[1] = EMF + CT + update.
+void oracle_region_flops(double out[2]) {
+  out[0] = oracle::g_region[0];
+  out[1] = oracle::g_region[1];
+}
 
 //---------------------------------------------------------------- pointwise ops
 static pmhd_mesh_desc desc_for(double gamma, int riemann, int limiter) {

@@ -1009,11 +1009,15 @@ class Mesh {
              bool do_exchange = true) {
     for (auto& B : blocks) {
       const State<R>& in = (s == 1) ? B.A : B.B;
+      const double f0 = g_tally.total();
       c2p_all(B, in, bad);
       for (int dir = 0; dir < g.dim; ++dir) fluxes(B, in, dir, s == 2, dt);
+      const double f1 = g_tally.total();
       emfs(B);
       State<R>& out = (s == 1) ? B.B : B.A;
       update(B, B.A, out, (s == 1) ? 0.5 : 1.0, dt, bad, nfloor);
+      g_region[0] += f1 - f0;  // (tally only moves in counting meshes)
+      g_region[1] += g_tally.total() - f1;
     }
     if (do_exchange) exchange(s == 1);
   }

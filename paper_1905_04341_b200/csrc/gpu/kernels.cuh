@@ -68,6 +68,9 @@ struct HaloSlab {
 };
 void launch_halo_copy(double* const* dev_arrays, const KGeom& G, const HaloSlab& sl, double* buf,
                       int to_buf, cudaStream_t s);
+void launch_repack(double* dense, double* pitched, const KGeom& G, int e1, int e2, int e3,
+                   int to_dense, cudaStream_t s);
+void launch_bcc_dense(double* dense, const double* bf, const KGeom& G, int c, cudaStream_t s);
 
 // Launchers (kernels.cu).
 void launch_c2p_all(const DevBlock* blks, const KGeom& G, const KPhys& ph, int sel, DevRed* red,

@@ -21,23 +21,32 @@ namespace {
 
 constexpr int UX = 32, UY = 8, UTHR = 256;
 constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0-1 .. j1)
+#ifndef PMHD_UPDATE_SEG
+#define PMHD_UPDATE_SEG 16  // k planes marched by one CTA
+#endif
 
+// A CTA owns a 32 x 8 (i, j) column of cells and marches k through a segment
+// [kb, kb + SEG).  What a plane shares with the next is carried instead of
+// recomputed: the cell-centred E ring holds planes k and k+1 (one new plane
+// loaded per step), E1 / E2 at k+1/2 become the k-1/2 values of the next
+// step, and so does the new b3 face at k+1.
 __global__ void __launch_bounds__(UTHR, 4)
 k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, DevRed* red,
                int want_dt, int kr0, int kr1) {
-  __shared__ double ec[3][3][EY][EX];      // [component][plane k-1,k,k+1][j][i]
+  __shared__ double ec[3][2][EY][EX];      // [component][k & 1][j][i]
   __shared__ double e3s[UY + 1][UX + 1];   // E3 at (k, j-1/2, i-1/2)
-  __shared__ double e1s[2][UY + 1][UX];    // E1 at (k-1/2 / k+1/2, j-1/2, i)
-  __shared__ double e2s[2][UY][UX + 1];    // E2 at (k-1/2 / k+1/2, j, i-1/2)
+  __shared__ double e1s[2][UY + 1][UX];    // E1 at (k -/+ 1/2, j-1/2, i), slot by parity
+  __shared__ double e2s[2][UY][UX + 1];    // E2 at (k -/+ 1/2, j, i-1/2)
   __shared__ double b1s[UY][UX + 1];
   __shared__ double b2s[UY + 1][UX];
-  __shared__ double b3s[2][UY][UX];
+  __shared__ double b3s[2][UY][UX];        // new b3 at faces k / k+1, slot by parity
   __shared__ double redbuf[UTHR / 32];
 
   const bool d3 = (G.dim == 3);
-  const int nk = kr1 - kr0;  // k planes [kr0, kr1) of this launch (a slab)
-  const int b = blockIdx.z / nk;
-  const int k = kr0 + (int)(blockIdx.z % nk);
+  const int nseg = (kr1 - kr0 + PMHD_UPDATE_SEG - 1) / PMHD_UPDATE_SEG;
+  const int b = blockIdx.z / nseg;
+  const int kb = kr0 + (int)(blockIdx.z % nseg) * PMHD_UPDATE_SEG;
+  const int kend = min(kb + PMHD_UPDATE_SEG, kr1);
   const int i0 = G.is + blockIdx.x * UX, j0 = G.js + blockIdx.y * UY;
   const int nx = min(UX, G.ie - i0), ny = min(UY, G.je - j0);
   const DevBlock& B = blks[b];
@@ -48,146 +57,171 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   double* const* X3 = B.fx[2];
   const int sx = G.sx, sy = G.sy;
   const int tid = threadIdx.x;
-
-  // ---- P1: cell-centred E of the stage-input state ------------------------
-  const int npl = d3 ? 3 : 1;
-#pragma unroll
-  for (int q = tid; q < 3 * EY * EX; q += UTHR) {
-    if (q >= npl * EY * EX) break;
-    const int c = q % EX, r = (q / EX) % EY, pl = q / (EX * EY);
-    const int ii = i0 - 1 + c, jj = j0 - 1 + r, kk = d3 ? k - 1 + pl : k;
-    const int ps = d3 ? pl : 1;
-    if (c > nx + 1 || r > ny + 1) continue;
-    const int id = G.idx(kk, jj, ii);
-    // written by the last-direction flux kernel from the same primitives
-    ec[0][ps][r][c] = __ldg(B.ec[0] + id);
-    ec[1][ps][r][c] = __ldg(B.ec[1] + id);
-    ec[2][ps][r][c] = __ldg(B.ec[2] + id);
-  }
-  __syncthreads();
-
-  // ---- P2: corner EMFs -------------------------------------------------------
   const int mode = ph.emf;
-#pragma unroll
-  for (int q = tid; q < (UY + 1) * (UX + 1); q += UTHR) {  // E3 at plane k
-    const int c = q % (UX + 1), r = q / (UX + 1);
-    if (c > nx || r > ny) continue;
-    const int id = G.idx(k, j0 + r, i0 + c);
-    const int ec_c = c + 1, ec_r = r + 1;
-    e3s[r][c] = corner_emf(mode, X1[5][id], X1[5][id - sx], X2[6][id], X2[6][id - 1], X1[7][id],
-                           X1[7][id - sx], X2[7][id], X2[7][id - 1], ec[2][1][ec_r][ec_c],
-                           ec[2][1][ec_r][ec_c - 1], ec[2][1][ec_r - 1][ec_c],
-                           ec[2][1][ec_r - 1][ec_c - 1]);
-  }
-#pragma unroll
-  for (int q = tid; q < 2 * (UY + 1) * UX; q += UTHR) {  // E1 at k-1/2, k+1/2
-    const int c = q % UX, r = (q / UX) % (UY + 1), h = q / (UX * (UY + 1));
-    if (c >= nx || r > ny) continue;
-    const int kk = k + h;
-    const int id = G.idx(d3 ? kk : k, j0 + r, i0 + c);
-    double e;
-    if (d3) {
-      const int pa = 1 + h, pm = h;  // Ec planes of kk and kk-1
-      e = corner_emf(mode, X2[5][id], X2[5][id - sy], X3[6][id], X3[6][id - sx], X2[7][id],
-                     X2[7][id - sy], X3[7][id], X3[7][id - sx], ec[0][pa][r + 1][c + 1],
-                     ec[0][pa][r][c + 1], ec[0][pm][r + 1][c + 1], ec[0][pm][r][c + 1]);
-    } else {
-      e = X2[5][id];
-    }
-    e1s[h][r][c] = e;
-  }
-#pragma unroll
-  for (int q = tid; q < 2 * UY * (UX + 1); q += UTHR) {  // E2 at k-1/2, k+1/2
-    const int c = q % (UX + 1), r = (q / (UX + 1)) % UY, h = q / ((UX + 1) * UY);
-    if (c > nx || r >= ny) continue;
-    const int kk = k + h;
-    const int id = G.idx(d3 ? kk : k, j0 + r, i0 + c);
-    double e;
-    if (d3) {
-      const int pa = 1 + h, pm = h;
-      e = corner_emf(mode, X3[5][id], X3[5][id - 1], X1[6][id], X1[6][id - sy], X3[7][id],
-                     X3[7][id - 1], X1[7][id], X1[7][id - sy], ec[1][pa][r + 1][c + 1],
-                     ec[1][pm][r + 1][c + 1], ec[1][pa][r + 1][c], ec[1][pm][r + 1][c]);
-    } else {
-      e = X1[6][id];
-    }
-    e2s[h][r][c] = e;
-  }
-  __syncthreads();
-
-  // ---- P3: constrained-transport face update ---------------------------------
   const double c1 = ks.c1, c2 = ks.c2, c3 = ks.c3;
-  for (int q = tid; q < UY * (UX + 1); q += UTHR) {  // b1f, faces i0 .. i0+nx
-    const int c = q % (UX + 1), r = q / (UX + 1);
-    if (c > nx || r >= ny) continue;
-    const int id = G.idx(k, j0 + r, i0 + c);
-    double v;
-    if (d3) v = Sb[5][id] - (c2 * (e3s[r + 1][c] - e3s[r][c]) - c3 * (e2s[1][r][c] - e2s[0][r][c]));
-    else v = Sb[5][id] - c2 * (e3s[r + 1][c] - e3s[r][c]);
-    b1s[r][c] = v;
-    if (c < nx || i0 + c == G.ie) Sout[5][id] = v;
-  }
-  for (int q = tid; q < (UY + 1) * UX; q += UTHR) {  // b2f, faces j0 .. j0+ny
-    const int c = q % UX, r = q / UX;
-    if (c >= nx || r > ny) continue;
-    const int id = G.idx(k, j0 + r, i0 + c);
-    double v;
-    if (d3) v = Sb[6][id] - (c3 * (e1s[1][r][c] - e1s[0][r][c]) - c1 * (e3s[r][c + 1] - e3s[r][c]));
-    else v = Sb[6][id] + c1 * (e3s[r][c + 1] - e3s[r][c]);
-    b2s[r][c] = v;
-    if (r < ny || j0 + r == G.je) Sout[6][id] = v;
-  }
-  for (int q = tid; q < 2 * UY * UX; q += UTHR) {  // b3f, faces k and k+1
-    const int c = q % UX, r = (q / UX) % UY, h = q / (UX * UY);
-    if (c >= nx || r >= ny) continue;
-    const int id = G.idx(k + h, j0 + r, i0 + c);
-    const double v = Sb[7][id] - (c1 * (e2s[h][r][c + 1] - e2s[h][r][c]) -
-                                  c2 * (e1s[h][r + 1][c] - e1s[h][r][c]));
-    b3s[h][r][c] = v;
-    if (h == 0 || k + 1 == G.ke) Sout[7][id] = v;
-  }
-  __syncthreads();
 
-  // ---- P4: conserved update + end-of-stage cons_to_prim + dt ----------------
+  // cell-centred E of plane kk (written by the last-direction flux kernel
+  // from the stage-input primitives) into ring slot kk & 1
+  auto load_ec = [&](int kk) {
+    const int sl = kk & 1;
+#pragma unroll
+    for (int q = tid; q < EY * EX; q += UTHR) {
+      const int c = q % EX, r = q / EX;
+      if (c > nx + 1 || r > ny + 1) continue;
+      const int id = G.idx(kk, j0 - 1 + r, i0 - 1 + c);
+      ec[0][sl][r][c] = __ldg(B.ec[0] + id);
+      ec[1][sl][r][c] = __ldg(B.ec[1] + id);
+      ec[2][sl][r][c] = __ldg(B.ec[2] + id);
+    }
+  };
+  // E1 / E2 on the edge plane kk - 1/2 (3D; in 2D the face E of plane k)
+  // into slot h
+  auto edge_emfs = [&](int kk, int h) {
+    const int pa = kk & 1, pm = (kk - 1) & 1;  // Ec slots of kk and kk-1
+#pragma unroll
+    for (int q = tid; q < (UY + 1) * UX; q += UTHR) {
+      const int c = q % UX, r = q / UX;
+      if (c >= nx || r > ny) continue;
+      const int id = G.idx(d3 ? kk : kb, j0 + r, i0 + c);
+      double e;
+      if (d3) {
+        e = corner_emf(mode, X2[5][id], X2[5][id - sy], X3[6][id], X3[6][id - sx], X2[7][id],
+                       X2[7][id - sy], X3[7][id], X3[7][id - sx], ec[0][pa][r + 1][c + 1],
+                       ec[0][pa][r][c + 1], ec[0][pm][r + 1][c + 1], ec[0][pm][r][c + 1]);
+      } else {
+        e = X2[5][id];
+      }
+      e1s[h][r][c] = e;
+    }
+#pragma unroll
+    for (int q = tid; q < UY * (UX + 1); q += UTHR) {
+      const int c = q % (UX + 1), r = q / (UX + 1);
+      if (c > nx || r >= ny) continue;
+      const int id = G.idx(d3 ? kk : kb, j0 + r, i0 + c);
+      double e;
+      if (d3) {
+        e = corner_emf(mode, X3[5][id], X3[5][id - 1], X1[6][id], X1[6][id - sy], X3[7][id],
+                       X3[7][id - 1], X1[7][id], X1[7][id - sy], ec[1][pa][r + 1][c + 1],
+                       ec[1][pm][r + 1][c + 1], ec[1][pa][r + 1][c], ec[1][pm][r + 1][c]);
+      } else {
+        e = X1[6][id];
+      }
+      e2s[h][r][c] = e;
+    }
+  };
+  // new b3 on face plane kk from the edge EMFs in slot h
+  auto face_b3 = [&](int kk, int h) {
+#pragma unroll
+    for (int q = tid; q < UY * UX; q += UTHR) {
+      const int c = q % UX, r = q / UX;
+      if (c >= nx || r >= ny) continue;
+      const int id = G.idx(kk, j0 + r, i0 + c);
+      const double v = Sb[7][id] - (c1 * (e2s[h][r][c + 1] - e2s[h][r][c]) -
+                                    c2 * (e1s[h][r + 1][c] - e1s[h][r][c]));
+      b3s[h][r][c] = v;
+    }
+  };
+
+  // ---- prologue: Ec planes kb-1, kb and the edge EMFs at kb - 1/2 ----------
+  if (d3) load_ec(kb - 1);
+  load_ec(kb);
+  __syncthreads();
+  edge_emfs(kb, kb & 1);
+  __syncthreads();
+  face_b3(kb, kb & 1);
+
   double tmin = 1.0e300;
-  {
-    const int c = tid % UX, r = tid / UX;
-    if (c < nx && r < ny) {
-      const int i = i0 + c, j = j0 + r;
-      const int id = G.idx(k, j, i);
-      double u[5];
+  for (int k = kb; k < kend; ++k) {
+    const int lo = k & 1, hi = lo ^ 1;  // slots of k - 1/2 and k + 1/2
+    // ---- A: the next Ec plane (slot of k-1, no longer needed) --------------
+    if (d3) load_ec(k + 1);
+    __syncthreads();
+    // ---- B: E3 at plane k, E1 / E2 at k + 1/2 -------------------------------
 #pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        double du = c1 * (X1[v][id + 1] - X1[v][id]) + c2 * (X2[v][id + sx] - X2[v][id]);
-        if (d3) du = du + c3 * (X3[v][id + sy] - X3[v][id]);
-        u[v] = Sb[v][id] - du;
+    for (int q = tid; q < (UY + 1) * (UX + 1); q += UTHR) {
+      const int c = q % (UX + 1), r = q / (UX + 1);
+      if (c > nx || r > ny) continue;
+      const int id = G.idx(k, j0 + r, i0 + c);
+      const int ec_c = c + 1, ec_r = r + 1;
+      e3s[r][c] = corner_emf(mode, X1[5][id], X1[5][id - sx], X2[6][id], X2[6][id - 1], X1[7][id],
+                             X1[7][id - sx], X2[7][id], X2[7][id - 1], ec[2][lo][ec_r][ec_c],
+                             ec[2][lo][ec_r][ec_c - 1], ec[2][lo][ec_r - 1][ec_c],
+                             ec[2][lo][ec_r - 1][ec_c - 1]);
+    }
+    edge_emfs(k + 1, hi);
+    __syncthreads();
+    // ---- C: constrained-transport face update -------------------------------
+    for (int q = tid; q < UY * (UX + 1); q += UTHR) {  // b1f, faces i0 .. i0+nx
+      const int c = q % (UX + 1), r = q / (UX + 1);
+      if (c > nx || r >= ny) continue;
+      const int id = G.idx(k, j0 + r, i0 + c);
+      double v;
+      if (d3) v = Sb[5][id] - (c2 * (e3s[r + 1][c] - e3s[r][c]) - c3 * (e2s[hi][r][c] - e2s[lo][r][c]));
+      else v = Sb[5][id] - c2 * (e3s[r + 1][c] - e3s[r][c]);
+      b1s[r][c] = v;
+      if (c < nx || i0 + c == G.ie) Sout[5][id] = v;
+    }
+    for (int q = tid; q < (UY + 1) * UX; q += UTHR) {  // b2f, faces j0 .. j0+ny
+      const int c = q % UX, r = q / UX;
+      if (c >= nx || r > ny) continue;
+      const int id = G.idx(k, j0 + r, i0 + c);
+      double v;
+      if (d3) v = Sb[6][id] - (c3 * (e1s[hi][r][c] - e1s[lo][r][c]) - c1 * (e3s[r][c + 1] - e3s[r][c]));
+      else v = Sb[6][id] + c1 * (e3s[r][c + 1] - e3s[r][c]);
+      b2s[r][c] = v;
+      if (r < ny || j0 + r == G.je) Sout[6][id] = v;
+    }
+    face_b3(k + 1, hi);  // b3 at face k + 1 (face k carried)
+    {
+      const int c = tid % UX, r = tid / UX;
+      if (c < nx && r < ny) {
+        const int id = G.idx(k, j0 + r, i0 + c);
+        Sout[7][id] = b3s[lo][r][c];
+        if (k + 1 == G.ke) Sout[7][id + sy] = b3s[hi][r][c];
       }
-      double bc[3], w[8];
-      bc[0] = 0.5 * (b1s[r][c] + b1s[r][c + 1]);
-      bc[1] = 0.5 * (b2s[r][c] + b2s[r + 1][c]);
-      bc[2] = 0.5 * (b3s[0][r][c] + b3s[1][r][c]);
-      const int fl = cons_to_prim(u, bc, ph, w, true);
-      if (fl & 3)
-        atomicAdd(&red[ks.stage].floor_count,
-                  (unsigned long long)(((fl & 1) ? 1 : 0) + ((fl & 2) ? 1 : 0)));
-      if (fl & 4) {
-        const long long gi = (long long)B.c[0] * G.mb[0] + (i - G.is);
-        const long long gj = (long long)B.c[1] * G.mb[1] + (j - G.js);
-        const long long gk = d3 ? (long long)B.c[2] * G.mb[2] + (k - G.ks) : 0;
-        atomicMin(&red[ks.stage].bad_key, (unsigned long long)((gk * G.nx[1] + gj) * G.nx[0] + gi));
-      }
+    }
+    __syncthreads();
+
+    // ---- D: conserved update + end-of-stage cons_to_prim + dt --------------
+    {
+      const int c = tid % UX, r = tid / UX;
+      if (c < nx && r < ny) {
+        const int i = i0 + c, j = j0 + r;
+        const int id = G.idx(k, j, i);
+        double u[5];
 #pragma unroll
-      for (int v = 0; v < 5; ++v) Sout[v][id] = u[v];
-      if (want_dt) {
-        const double d = w[0], p = w[4];
-        const double cf1 = fast_speed_n(d, p, w[5], w[6], w[7], ph.gamma);
-        const double cf2 = fast_speed_n(d, p, w[6], w[7], w[5], ph.gamma);
-        double t = fmin(G.dx[0] / (fabs(w[1]) + cf1), G.dx[1] / (fabs(w[2]) + cf2));
-        if (d3) {
-          const double cf3 = fast_speed_n(d, p, w[7], w[5], w[6], ph.gamma);
-          t = fmin(t, G.dx[2] / (fabs(w[3]) + cf3));
+        for (int v = 0; v < 5; ++v) {
+          double du = c1 * (X1[v][id + 1] - X1[v][id]) + c2 * (X2[v][id + sx] - X2[v][id]);
+          if (d3) du = du + c3 * (X3[v][id + sy] - X3[v][id]);
+          u[v] = Sb[v][id] - du;
         }
-        tmin = t;
+        double bc[3], w[8];
+        bc[0] = 0.5 * (b1s[r][c] + b1s[r][c + 1]);
+        bc[1] = 0.5 * (b2s[r][c] + b2s[r + 1][c]);
+        bc[2] = 0.5 * (b3s[lo][r][c] + b3s[hi][r][c]);
+        const int fl = cons_to_prim(u, bc, ph, w, true);
+        if (fl & 3)
+          atomicAdd(&red[ks.stage].floor_count,
+                    (unsigned long long)(((fl & 1) ? 1 : 0) + ((fl & 2) ? 1 : 0)));
+        if (fl & 4) {
+          const long long gi = (long long)B.c[0] * G.mb[0] + (i - G.is);
+          const long long gj = (long long)B.c[1] * G.mb[1] + (j - G.js);
+          const long long gk = d3 ? (long long)B.c[2] * G.mb[2] + (k - G.ks) : 0;
+          atomicMin(&red[ks.stage].bad_key, (unsigned long long)((gk * G.nx[1] + gj) * G.nx[0] + gi));
+        }
+#pragma unroll
+        for (int v = 0; v < 5; ++v) Sout[v][id] = u[v];
+        if (want_dt) {
+          const double d = w[0], p = w[4];
+          const double cf1 = fast_speed_n(d, p, w[5], w[6], w[7], ph.gamma);
+          const double cf2 = fast_speed_n(d, p, w[6], w[7], w[5], ph.gamma);
+          double t = fmin(G.dx[0] / (fabs(w[1]) + cf1), G.dx[1] / (fabs(w[2]) + cf2));
+          if (d3) {
+            const double cf3 = fast_speed_n(d, p, w[7], w[5], w[6], ph.gamma);
+            t = fmin(t, G.dx[2] / (fabs(w[3]) + cf3));
+          }
+          tmin = fmin(tmin, t);
+        }
       }
     }
   }
@@ -207,7 +241,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
 
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                          DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s) {
-  const dim3 grid((G.ie - G.is + UX - 1) / UX, (G.je - G.js + UY - 1) / UY, (kr1 - kr0) * G.nb);
+  const int nseg = (kr1 - kr0 + PMHD_UPDATE_SEG - 1) / PMHD_UPDATE_SEG;
+  const dim3 grid((G.ie - G.is + UX - 1) / UX, (G.je - G.js + UY - 1) / UY, nseg * G.nb);
   k_update_fused<<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);
 }
 

@@ -253,18 +253,6 @@ int finish(pmhd_mesh* m, int stage_lo, int stage_hi, double* dt_next, pmhd_statu
   return PMHD_OK;
 }
 
-int copy3d(pmhd_ctx* ctx, void* dst, size_t dpitch, size_t dy, const void* src, size_t spitch,
-           size_t sy, size_t wbytes, size_t h, size_t d, cudaMemcpyKind kind) {
-  cudaMemcpy3DParms p;
-  std::memset(&p, 0, sizeof(p));
-  p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), spitch, wbytes / sizeof(double), sy);
-  p.dstPtr = make_cudaPitchedPtr(dst, dpitch, wbytes / sizeof(double), dy);
-  p.extent = make_cudaExtent(wbytes, h, d);
-  p.kind = kind;
-  CK(cudaMemcpy3DAsync(&p, ctx->stream));
-  return PMHD_OK;
-}
-
 int local_index(const pmhd_mesh* m, int gid) {
   for (size_t b = 0; b < m->gids.size(); ++b)
     if (m->gids[b] == gid) return int(b);
@@ -449,6 +437,24 @@ int pmhd_gpu_block_dims(const pmhd_mesh* m, int n[3]) {
   return PMHD_OK;
 }
 
+// One array between a dense host buffer (e1 x e2 x e3, i fastest) and a
+// pitched block array, staged through a contiguous device buffer: one large
+// PCIe DMA (full speed from pinned memory) plus an HBM-speed repack kernel.
+static int xfer(pmhd_ctx* ctx, const KGeom& G, double* host, double* dev, double* stg, int e1,
+                int e2, int e3, bool to_host) {
+  const size_t bytes = size_t(e1) * e2 * e3 * sizeof(double);
+  if (to_host) {
+    launch_repack(stg, dev, G, e1, e2, e3, 1, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(host, stg, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    CK(cudaMemcpyAsync(stg, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    launch_repack(stg, dev, G, e1, e2, e3, 0, ctx->stream);
+    CK(cudaGetLastError());
+  }
+  return PMHD_OK;
+}
+
 int pmhd_gpu_upload_block(pmhd_mesh* m, int gid, const double* u, const double* b1f,
                           const double* b2f, const double* b3f) {
   if (!m) return PMHD_ERR_INPUT;
@@ -457,20 +463,15 @@ int pmhd_gpu_upload_block(pmhd_mesh* m, int gid, const double* u, const double* 
   if (b < 0) return fail(ctx, PMHD_ERR_INPUT, "block not local");
   if (!u || !b1f || !b2f || !b3f) return fail(ctx, PMHD_ERR_BUFFER, "null buffer");
   const KGeom& G = m->G;
-  const size_t dp = size_t(G.sx) * sizeof(double), dy = size_t(G.n2 + 1);
   const size_t nc = size_t(G.n1) * G.n2 * G.n3;
   DevBlock& B = m->hblk[b];
-  for (int v = 0; v < 5; ++v) {
-    int rc = copy3d(ctx, B.st[0][v], dp, dy, u + v * nc, G.n1 * sizeof(double), G.n2,
-                    G.n1 * sizeof(double), G.n2, G.n3, cudaMemcpyHostToDevice);
-    if (rc) return rc;
-  }
-  int rc = copy3d(ctx, B.st[0][5], dp, dy, b1f, (G.n1 + 1) * sizeof(double), G.n2,
-                  (G.n1 + 1) * sizeof(double), G.n2, G.n3, cudaMemcpyHostToDevice);
-  if (!rc) rc = copy3d(ctx, B.st[0][6], dp, dy, b2f, G.n1 * sizeof(double), G.n2 + 1,
-                       G.n1 * sizeof(double), G.n2 + 1, G.n3, cudaMemcpyHostToDevice);
-  if (!rc) rc = copy3d(ctx, B.st[0][7], dp, dy, b3f, G.n1 * sizeof(double), G.n2,
-                       G.n1 * sizeof(double), G.n2, G.n3 + 1, cudaMemcpyHostToDevice);
+  double* stg = B.fx[0][0];  // face-data scratch: free outside a stage
+  double* hu = const_cast<double*>(u);
+  int rc = PMHD_OK;
+  for (int v = 0; v < 5 && !rc; ++v) rc = xfer(ctx, G, hu + v * nc, B.st[0][v], stg, G.n1, G.n2, G.n3, false);
+  if (!rc) rc = xfer(ctx, G, const_cast<double*>(b1f), B.st[0][5], stg, G.n1 + 1, G.n2, G.n3, false);
+  if (!rc) rc = xfer(ctx, G, const_cast<double*>(b2f), B.st[0][6], stg, G.n1, G.n2 + 1, G.n3, false);
+  if (!rc) rc = xfer(ctx, G, const_cast<double*>(b3f), B.st[0][7], stg, G.n1, G.n2, G.n3 + 1, false);
   if (rc) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
   return PMHD_OK;
@@ -483,53 +484,31 @@ int pmhd_gpu_download_block(pmhd_mesh* m, int gid, double* u, double* w, double*
   const int b = local_index(m, gid);
   if (b < 0) return fail(ctx, PMHD_ERR_INPUT, "block not local");
   const KGeom& G = m->G;
-  const size_t dp = size_t(G.sx) * sizeof(double), dy = size_t(G.n2 + 1);
   const size_t nc = size_t(G.n1) * G.n2 * G.n3;
   DevBlock& B = m->hblk[b];
-  std::vector<double> f1, f2, f3;
-  double* p1 = b1f;
-  double* p2 = b2f;
-  double* p3 = b3f;
-  if (u) {  // Bcc needs the faces
-    if (!p1) { f1.resize(size_t(G.n3) * G.n2 * (G.n1 + 1)); p1 = f1.data(); }
-    if (!p2) { f2.resize(size_t(G.n3) * (G.n2 + 1) * G.n1); p2 = f2.data(); }
-    if (!p3) { f3.resize(size_t(G.n3 + 1) * G.n2 * G.n1); p3 = f3.data(); }
-  }
+  double* stg = B.fx[0][0];
   int rc = PMHD_OK;
-  if (u)
-    for (int v = 0; v < 5 && !rc; ++v)
-      rc = copy3d(ctx, u + v * nc, G.n1 * sizeof(double), G.n2, B.st[0][v], dp, dy,
-                  G.n1 * sizeof(double), G.n2, G.n3, cudaMemcpyDeviceToHost);
-  if (p1 && !rc) rc = copy3d(ctx, p1, (G.n1 + 1) * sizeof(double), G.n2, B.st[0][5], dp, dy,
-                             (G.n1 + 1) * sizeof(double), G.n2, G.n3, cudaMemcpyDeviceToHost);
-  if (p2 && !rc) rc = copy3d(ctx, p2, G.n1 * sizeof(double), G.n2 + 1, B.st[0][6], dp, dy,
-                             G.n1 * sizeof(double), G.n2 + 1, G.n3, cudaMemcpyDeviceToHost);
-  if (p3 && !rc) rc = copy3d(ctx, p3, G.n1 * sizeof(double), G.n2, B.st[0][7], dp, dy,
-                             G.n1 * sizeof(double), G.n2, G.n3 + 1, cudaMemcpyDeviceToHost);
+  if (u) {
+    for (int v = 0; v < 5 && !rc; ++v) rc = xfer(ctx, G, u + v * nc, B.st[0][v], stg, G.n1, G.n2, G.n3, true);
+    // face_to_center_b on the device, same IEEE operations
+    for (int c = 0; c < 3 && !rc; ++c) {
+      launch_bcc_dense(stg, B.st[0][5 + c], G, c, ctx->stream);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(u + (5 + c) * nc, stg, nc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+  }
+  if (b1f && !rc) rc = xfer(ctx, G, b1f, B.st[0][5], stg, G.n1 + 1, G.n2, G.n3, true);
+  if (b2f && !rc) rc = xfer(ctx, G, b2f, B.st[0][6], stg, G.n1, G.n2 + 1, G.n3, true);
+  if (b3f && !rc) rc = xfer(ctx, G, b3f, B.st[0][7], stg, G.n1, G.n2, G.n3 + 1, true);
   if (rc) return rc;
   if (w) {
     rc = reset_red(m);
     if (rc) return rc;
     launch_c2p_all(m->dblk, G, m->ph, 0, m->dred, 0, ctx->stream);
-    for (int v = 0; v < 8 && !rc; ++v)
-      rc = copy3d(ctx, w + v * nc, G.n1 * sizeof(double), G.n2, B.w[v], dp, dy,
-                  G.n1 * sizeof(double), G.n2, G.n3, cudaMemcpyDeviceToHost);
+    for (int v = 0; v < 8 && !rc; ++v) rc = xfer(ctx, G, w + v * nc, B.w[v], stg, G.n1, G.n2, G.n3, true);
     if (rc) return rc;
   }
   CK(cudaStreamSynchronize(ctx->stream));
-  if (u) {  // face_to_center_b, same IEEE ops as the kernels
-    for (int k = 0; k < G.n3; ++k)
-      for (int j = 0; j < G.n2; ++j)
-        for (int i = 0; i < G.n1; ++i) {
-          const size_t c = (size_t(k) * G.n2 + j) * G.n1 + i;
-          const size_t q1 = (size_t(k) * G.n2 + j) * (G.n1 + 1) + i;
-          const size_t q2 = (size_t(k) * (G.n2 + 1) + j) * G.n1 + i;
-          const size_t q3 = (size_t(k) * G.n2 + j) * G.n1 + i;
-          u[5 * nc + c] = 0.5 * (p1[q1] + p1[q1 + 1]);
-          u[6 * nc + c] = 0.5 * (p2[q2] + p2[q2 + G.n1]);
-          u[7 * nc + c] = 0.5 * (p3[q3] + p3[q3 + size_t(G.n2) * G.n1]);
-        }
-  }
   return PMHD_OK;
 }
 

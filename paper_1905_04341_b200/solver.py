@@ -83,8 +83,10 @@ class GpuSolver:
         self._check(self.L.pmhd_gpu_upload_block(self.mesh, gid, N.dptr(b.u), N.dptr(b.b1f),
                                                  N.dptr(b.b2f), N.dptr(b.b3f)))
 
-    def get_block(self, gid, with_w=False):
-        b = BlockState.zeros(self.cfg.block_dims)
+    def get_block(self, gid, with_w=False, out: BlockState = None):
+        """Download block gid (Bcc re-derived from the faces).  out: an
+        existing BlockState to fill (e.g. pinned host buffers)."""
+        b = BlockState.zeros(self.cfg.block_dims) if out is None else out
         w = np.zeros_like(b.u) if with_w else None
         self._check(self.L.pmhd_gpu_download_block(self.mesh, gid, N.dptr(b.u), N.dptr(w),
                                                    N.dptr(b.b1f), N.dptr(b.b2f), N.dptr(b.b3f)))
