@@ -14,9 +14,10 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -Xlinker -Bsymbolic -std=c++17 -Xcompiler -fPI
             -Xptxas -warn-spills --expt-relaxed-constexpr
 HOSTFLAGS:= -std=c++20 -O2 -march=x86-64-v3 -fPIC -Wall -Wextra -Iinclude
 GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu $(GPUSRC)/kernels_flux.cu $(GPUSRC)/kernels_update.cu $(GPUSRC)/kernels_halo.cu
+FASTDS   := -DPMHD_FAST_DIVSQRT
 GPU_DEPS := $(GPU_SRCS) $(wildcard $(GPUSRC)/*.cuh) include/pmhd_gpu.h
 
-all: host gpu cli oracle
+all: host gpu cli oracle testlib
 
 host: $(LIB)/libpmhd_host.so
 gpu: $(LIB)/libpmhd_gpu.so $(LIB)/libpmhd_gpu_parity.so
@@ -27,11 +28,18 @@ $(LIB)/libpmhd_host.so: $(PKG)/csrc/host/pmhd_host.cpp $(PKG)/csrc/host/snapshot
 
 $(LIB)/libpmhd_gpu.so: $(GPU_DEPS)
 	@mkdir -p $(LIB)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPU_SRCS)
+	$(NVCC) $(NVFLAGS) $(FASTDS) -shared -o $@ $(GPU_SRCS)
 
 $(LIB)/libpmhd_gpu_parity.so: $(GPU_DEPS)
 	@mkdir -p $(LIB)
 	$(NVCC) $(NVFLAGS) --fmad=false -DPMHD_PARITY -shared -o $@ $(GPU_SRCS)
+
+# GPU test helper (tests/cuda): checks the product build's division / sqrt
+testlib: $(LIB)/test/libpmhd_divsqrt_check.so
+
+$(LIB)/test/libpmhd_divsqrt_check.so: tests/cuda/divsqrt_check.cu $(GPUSRC)/physics.cuh
+	@mkdir -p $(LIB)/test
+	$(NVCC) $(NVFLAGS) $(FASTDS) -shared -o $@ $<
 
 cli: $(PKG)/bin/pmhd
 
@@ -46,11 +54,11 @@ clean:
 	rm -f $(LIB)/*.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all host gpu cli oracle clean exp
+.PHONY: all host gpu cli oracle clean exp testlib
 
 # A/B experiment builds (bench.py honours PMHD_GPU_LIB=<path>)
 exp: $(GPU_DEPS)
 	@mkdir -p $(LIB)/exp
-	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_SMEMW=0 -DPMHD_FLUX_MINB=4 -shared -o $(LIB)/exp/libpmhd_gpu_regs.so $(GPU_SRCS)
-	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_MINB=4 -shared -o $(LIB)/exp/libpmhd_gpu_minb4.so $(GPU_SRCS)
-	$(NVCC) $(NVFLAGS) -DPMHD_FLUX_MINB=6 -shared -o $(LIB)/exp/libpmhd_gpu_minb6.so $(GPU_SRCS)
+	$(NVCC) $(NVFLAGS) $(FASTDS) -DPMHD_FLUX_SMEMW=0 -DPMHD_FLUX_MINB=4 -shared -o $(LIB)/exp/libpmhd_gpu_regs.so $(GPU_SRCS)
+	$(NVCC) $(NVFLAGS) $(FASTDS) -DPMHD_FLUX_MINB=4 -shared -o $(LIB)/exp/libpmhd_gpu_minb4.so $(GPU_SRCS)
+	$(NVCC) $(NVFLAGS) $(FASTDS) -DPMHD_FLUX_MINB=6 -shared -o $(LIB)/exp/libpmhd_gpu_minb6.so $(GPU_SRCS)

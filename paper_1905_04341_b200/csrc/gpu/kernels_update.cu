@@ -215,10 +215,10 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
           const double d = w[0], p = w[4];
           const double cf1 = fast_speed_n(d, p, w[5], w[6], w[7], ph.gamma);
           const double cf2 = fast_speed_n(d, p, w[6], w[7], w[5], ph.gamma);
-          double t = fmin(G.dx[0] / (fabs(w[1]) + cf1), G.dx[1] / (fabs(w[2]) + cf2));
+          double t = fmin(ddiv(G.dx[0], fabs(w[1]) + cf1), ddiv(G.dx[1], fabs(w[2]) + cf2));
           if (d3) {
             const double cf3 = fast_speed_n(d, p, w[7], w[5], w[6], ph.gamma);
-            t = fmin(t, G.dx[2] / (fabs(w[3]) + cf3));
+            t = fmin(t, ddiv(G.dx[2], fabs(w[3]) + cf3));
           }
           tmin = fmin(tmin, t);
         }

@@ -1,0 +1,39 @@
+"""The product build's branch-free division / square root (physics.cuh,
+PMHD_FAST_DIVSQRT) against the IEEE operators, bit for bit, over operands
+spanning the ranges the physics produces (and well beyond): 1e-30 .. 1e30,
+both signs, exact squares, powers of two, and sqrt(0)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_1905_04341_b200.native import LIB_DIR
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    path = LIB_DIR / "test" / "libpmhd_divsqrt_check.so"
+    if not path.exists():
+        pytest.fail(f"missing {path} (run __graft_entry__.build())")
+    L = C.CDLL(str(path))
+    L.pmhd_test_divsqrt.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]
+    return L
+
+
+def test_fast_divsqrt_bitwise_ieee(gpu_available):
+    rng = np.random.default_rng(1905)
+    n = 1 << 22
+    a = rng.choice([-1.0, 1.0], n) * 10.0 ** rng.uniform(-30, 30, n)
+    b = rng.choice([-1.0, 1.0], n) * 10.0 ** rng.uniform(-30, 30, n)
+    # physics-like magnitudes, exact cases and perfect squares
+    a[: n // 4] = rng.uniform(1e-3, 1e3, n // 4)
+    b[: n // 4] = rng.uniform(1e-3, 1e3, n // 4)
+    a[n // 4: n // 4 + 1000] = np.arange(1000, dtype=np.float64) ** 2
+    b[n // 4: n // 4 + 1000] = 2.0 ** rng.integers(-60, 60, 1000)
+    a[n // 4] = 0.0
+    out = np.zeros(2, dtype=np.uint64)
+    rc = _lib().pmhd_test_divsqrt(a.ctypes.data, b.ctypes.data, n, out.ctypes.data)
+    assert rc == 0
+    assert out[0] == 0, f"{out[0]} divisions differ from IEEE"
+    assert out[1] == 0, f"{out[1]} square roots differ from IEEE"
