@@ -15,7 +15,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -Xlinker -Bsymbolic -std=c++17 -Xcompiler -fPI
 HOSTFLAGS:= -std=c++20 -O2 -march=x86-64-v3 -fPIC -Wall -Wextra -Iinclude
 GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu $(GPUSRC)/kernels_flux.cu $(GPUSRC)/kernels_update.cu $(GPUSRC)/kernels_halo.cu
 FASTDS   := -DPMHD_FAST_DIVSQRT
-GPU_DEPS := $(GPU_SRCS) $(wildcard $(GPUSRC)/*.cuh) include/pmhd_gpu.h
+GPU_DEPS := $(GPU_SRCS) $(wildcard $(GPUSRC)/*.cuh) include/pmhd_gpu.h Makefile
 
 all: host gpu cli oracle testlib
 
