@@ -21,6 +21,9 @@ namespace {
 
 constexpr int UX = 32, UY = 8, UTHR = 256;
 constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0-1 .. j1)
+#ifndef PMHD_UPDATE_MINB
+#define PMHD_UPDATE_MINB 5  // resident CTAs per SM the register budget targets (48 regs)
+#endif
 #ifndef PMHD_UPDATE_SEG
 #define PMHD_UPDATE_SEG 16  // k planes marched by one CTA
 #endif
@@ -30,7 +33,7 @@ constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0
 // recomputed: the cell-centred E ring holds planes k and k+1 (one new plane
 // loaded per step), E1 / E2 at k+1/2 become the k-1/2 values of the next
 // step, and so does the new b3 face at k+1.
-__global__ void __launch_bounds__(UTHR, 4)
+__global__ void __launch_bounds__(UTHR, PMHD_UPDATE_MINB)
 k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, DevRed* red,
                int want_dt, int kr0, int kr1) {
   __shared__ double ec[3][2][EY][EX];      // [component][k & 1][j][i]
