@@ -369,18 +369,19 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   cudaMemsetAsync(m->slab, 0, bytes, ctx->stream);
   m->hblk.resize(G.nb);
   // Row alignment per array group: element i = shift of every row starts a
-  // 256 B segment.  State and cell-E rows are aligned at i = 1 (the first
+  // 256 B segment.  State and cell-E rows are aligned at i = is-1 (the first
   // cell the x2/x3 flux tiles and the update's E box touch), face-data rows at
-  // i = 2 = is (the update tiles' first face); measured best of the (0..2)^3
+  // i = is (the update tiles' first face); measured best of the (0..2)^3
   // combinations on B200 (+4.7 % over unshifted).  PMHD_ROW_SHIFT[_ST|_FX|_EC]
   // override for experiments.
   auto shift_env = [](const char* k, int d) {
     const char* v = std::getenv(k);
     return v ? std::max(0, std::min(31, std::atoi(v))) : d;
   };
-  const int sh_st = shift_env("PMHD_ROW_SHIFT_ST", shift_env("PMHD_ROW_SHIFT", 1));
-  const int sh_fx = shift_env("PMHD_ROW_SHIFT_FX", shift_env("PMHD_ROW_SHIFT", 2));
-  const int sh_ec = shift_env("PMHD_ROW_SHIFT_EC", shift_env("PMHD_ROW_SHIFT", 1));
+  const int a1 = std::min(31, G.ng - 1), a2 = std::min(31, G.ng);  // i = is-1, i = is
+  const int sh_st = shift_env("PMHD_ROW_SHIFT_ST", shift_env("PMHD_ROW_SHIFT", a1));
+  const int sh_fx = shift_env("PMHD_ROW_SHIFT_FX", shift_env("PMHD_ROW_SHIFT", a2));
+  const int sh_ec = shift_env("PMHD_ROW_SHIFT_EC", shift_env("PMHD_ROW_SHIFT", a1));
   for (int b = 0; b < G.nb; ++b) {
     double* p = m->slab + size_t(b) * per_block + 32;
     DevBlock& B = m->hblk[b];
