@@ -179,6 +179,14 @@ int pmhd_gpu_halo_count(const pmhd_mesh* mesh, int dir, int side, long long* n);
 int pmhd_gpu_halo_pack(pmhd_mesh* mesh, int gid, int dir, int side, int half, double* dev_buf);
 /* ghosts of block gid on `side`, from the neighbour's pack(..., 1 - side) */
 int pmhd_gpu_halo_unpack(pmhd_mesh* mesh, int gid, int dir, int side, int half, const double* dev_buf);
+/* Stream-ordered multi-rank mode (on != 0): exchange_dir / halo_pack /
+ * halo_unpack return as soon as their kernels are enqueued on
+ * pmhd_gpu_stream(ctx), and stage_compute(1) returns without synchronizing
+ * (its floor count / error cell are reported by the following
+ * stage_compute(2), whose status covers both stages).  The transport must
+ * order its device work on that stream (e.g. NCCL issued on it).  Off
+ * (default): every call returns once its results are complete. */
+int pmhd_gpu_set_async(pmhd_mesh* mesh, int on);
 
 /* Diagnostics (PMHD_DIAG_*). */
 int pmhd_gpu_diag(pmhd_mesh* mesh, int kind, double* out);

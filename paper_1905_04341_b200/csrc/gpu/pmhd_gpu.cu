@@ -53,6 +53,7 @@ struct pmhd_mesh {
   double* drows = nullptr;
   bool all_local = true;
   bool prof = false;
+  bool async_ops = false;         // pmhd_gpu_set_async: stream-ordered multi-rank calls
   int variant = 0;                // 0: fused flux kernels; 1: split (debug; PMHD_KERNELS=split)
   int slab_planes = 0;            // k-slab pipeline depth (PMHD_SLAB_PLANES, 0 = off)
   std::vector<cudaEvent_t> slab_ev;
@@ -674,10 +675,26 @@ HaloSlab make_slab(const KGeom& G, int dir, int side, bool send) {
 int pmhd_gpu_stage_compute(pmhd_mesh* m, int stage, double dt, double* dt_next, pmhd_status* st) {
   if (!m) return PMHD_ERR_INPUT;
   if (stage != 1 && stage != 2) return fail(m->ctx, PMHD_ERR_INPUT, "stage must be 1 or 2");
+  if (m->async_ops) {  // reductions of both stages are checked after stage 2
+    int rc = (stage == 1) ? reset_red(m) : PMHD_OK;
+    if (!rc) rc = enqueue_stage(m, stage, dt, false);
+    if (rc) return rc;
+    if (stage == 1) {
+      if (st) { std::memset(st, 0, sizeof(*st)); st->k = st->j = st->i = -1; st->stage = 1; }
+      return PMHD_OK;
+    }
+    return finish(m, 1, 2, dt_next, st);
+  }
   int rc = reset_red(m);
   if (!rc) rc = enqueue_stage(m, stage, dt, false);
   if (rc) return rc;
   return finish(m, stage, stage, stage == 2 ? dt_next : nullptr, st);
+}
+
+int pmhd_gpu_set_async(pmhd_mesh* m, int on) {
+  if (!m) return PMHD_ERR_INPUT;
+  m->async_ops = on != 0;
+  return PMHD_OK;
 }
 
 int pmhd_gpu_exchange_dir(pmhd_mesh* m, int dir, int half) {
@@ -686,7 +703,7 @@ int pmhd_gpu_exchange_dir(pmhd_mesh* m, int dir, int half) {
   launch_exchange_dir(m->dblk, m->G, half ? 1 : 0, dir, ctx->stream);
   m->times.kernel_launches += 1;
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(ctx->stream));
+  if (!m->async_ops) CK(cudaStreamSynchronize(ctx->stream));
   return PMHD_OK;
 }
 
@@ -706,7 +723,7 @@ static int halo_xfer(pmhd_mesh* m, int gid, int dir, int side, int half, double*
   launch_halo_copy(arrays, m->G, sl, dev_buf, pack ? 1 : 0, ctx->stream);
   m->times.kernel_launches += 1;
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(ctx->stream));
+  if (!m->async_ops) CK(cudaStreamSynchronize(ctx->stream));
   return PMHD_OK;
 }
 

@@ -152,7 +152,7 @@ GPU_SYMBOLS = [
     "pmhd_gpu_exchange", "pmhd_gpu_new_dt", "pmhd_gpu_stage", "pmhd_gpu_vl2_step",
     "pmhd_gpu_run", "pmhd_gpu_diag", "pmhd_gpu_set_profiling", "pmhd_gpu_region_times",
     "pmhd_gpu_build_info", "pmhd_gpu_stream", "pmhd_gpu_stage_compute", "pmhd_gpu_exchange_dir",
-    "pmhd_gpu_halo_count", "pmhd_gpu_halo_pack", "pmhd_gpu_halo_unpack",
+    "pmhd_gpu_halo_count", "pmhd_gpu_halo_pack", "pmhd_gpu_halo_unpack", "pmhd_gpu_set_async",
 ]
 
 
@@ -197,6 +197,7 @@ def gpu_lib(parity: bool = False) -> C.CDLL:
         L.pmhd_gpu_halo_count.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_longlong)]
         L.pmhd_gpu_halo_pack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.pmhd_gpu_halo_unpack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.pmhd_gpu_set_async.argtypes = [C.c_void_p, C.c_int]
         L.pmhd_gpu_stream.argtypes = [C.c_void_p]
         L.pmhd_gpu_stream.restype = C.c_void_p
         L.pmhd_gpu_build_info.argtypes = []

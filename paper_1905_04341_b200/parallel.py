@@ -109,9 +109,15 @@ class TorchDistTransport:
         # send CUDA tensors); used to validate the multi-rank GPU path with
         # several processes on one GPU, never for measurements.
         self.host_staging = host_staging
+        # NCCL on CUDA buffers can be ordered on the engine's stream: no host
+        # synchronization inside a stage (DistributedVL2 enables it).
+        self.stream_ordered = (not host_staging) and dist.get_backend(group) == "nccl"
 
-    def exchange(self, out, inb):
-        """out / inb: lists of (peer, tensor) in posting order."""
+    def exchange(self, out, inb, stream=None):
+        """out / inb: lists of (peer, tensor) in posting order.  stream: a
+        torch stream the transfers are ordered on (stream_ordered transports):
+        they start after the work already enqueued on it and later work on it
+        waits for them, without blocking the host."""
         if self.host_staging:
             out = [(p, t.cpu()) for p, t in out]
             tmp = [(p, t, t.new_empty(t.shape, device="cpu")) for p, t in inb]
@@ -120,7 +126,12 @@ class TorchDistTransport:
             inb_x = inb
         ops = [self.dist.P2POp(self.dist.isend, t, p, group=self.group) for p, t in out]
         ops += [self.dist.P2POp(self.dist.irecv, t, p, group=self.group) for p, t in inb_x]
-        if ops:
+        if ops and stream is not None:
+            import torch
+            with torch.cuda.stream(stream):
+                for req in self.dist.batch_isend_irecv(ops):
+                    req.wait()  # NCCL: the stream waits, the host does not
+        elif ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
             # NCCL completes on torch's current stream; the ABI unpacks on its
@@ -159,6 +170,14 @@ class DistributedVL2:
             for peer, key in recvs:
                 b.recv[key] = engine.alloc_halo(engine.halo_count(d, key[1]))
             self.bufs[d] = (sends, recvs, b)
+        # stream-ordered stages: pack -> NCCL -> unpack all on the engine's
+        # stream; the host synchronizes once per cycle (stage 2 status + dt)
+        self.stream = None
+        import os
+        if (getattr(transport, "stream_ordered", False) and hasattr(engine, "set_async")
+                and os.environ.get("PMHD_SYNC_HALO", "0") != "1"):
+            engine.set_async(True)
+            self.stream = engine.torch_stream()
 
     def exchange(self, half):
         for d in range(self.plan.dim):
@@ -166,7 +185,8 @@ class DistributedVL2:
             sends, recvs, b = self.bufs[d]
             for peer, key, gid, side in sends:
                 self.e.halo_pack(gid, d, side, half, b.send[key])
-            self.tr.exchange([(p, b.send[k]) for p, k, _, _ in sends], [(p, b.recv[k]) for p, k in recvs])
+            self.tr.exchange([(p, b.send[k]) for p, k, _, _ in sends], [(p, b.recv[k]) for p, k in recvs],
+                             stream=self.stream)
             for peer, key in recvs:
                 self.e.halo_unpack(key[0], d, key[1], half, b.recv[key])
 
@@ -183,12 +203,62 @@ class DistributedVL2:
 
 class LoopbackWorld:
     """Several rank engines in ONE process, stepped in lockstep; messages are
-    handed over by device/host copies.  Nothing waits on another kernel."""
+    handed over by device/host copies.  Nothing waits on another kernel.
 
-    def __init__(self, engines, plan):
+    stream_ordered=True puts the engines in pmhd_gpu_set_async mode and orders
+    the hand-over with CUDA events between the engines' streams, the way NCCL
+    orders send/recv on the issuing stream (DistributedVL2 over NCCL): the
+    host never synchronizes inside a stage."""
+
+    def __init__(self, engines, plan, stream_ordered=False):
         self.engines, self.plan = engines, plan
+        self.stream_ordered = stream_ordered
+        if stream_ordered:
+            for e in engines:
+                e.set_async(True)
+            self.streams = [e.torch_stream() for e in engines]
+            self.send, self.recv = {}, {}
+            for d in range(plan.dim):
+                for r, e in enumerate(engines):
+                    sends, recvs = plan.messages(r, d)
+                    for peer, key, gid, side in sends:
+                        self.send[(d, peer, key)] = e.alloc_halo(e.halo_count(d, 1 - side))
+                    for peer, key in recvs:
+                        self.recv[(d, r, key)] = e.alloc_halo(e.halo_count(d, key[1]))
+
+    def _exchange_streams(self, half):
+        import torch
+        n = len(self.engines)
+        for d in range(self.plan.dim):
+            for r, e in enumerate(self.engines):
+                e.exchange_dir(d, half)
+                sends, _ = self.plan.messages(r, d)
+                for peer, key, gid, side in sends:
+                    e.halo_pack(gid, d, side, half, self.send[(d, peer, key)])
+            packed = [torch.cuda.Event() for _ in range(n)]
+            for r in range(n):
+                packed[r].record(self.streams[r])
+            for r, e in enumerate(self.engines):
+                _, recvs = self.plan.messages(r, d)
+                for peer, key in recvs:
+                    self.streams[r].wait_event(packed[peer])
+                    dst = self.recv[(d, r, key)]
+                    with torch.cuda.stream(self.streams[r]):
+                        dst.copy_(self.send[(d, r, key)])
+                    e.halo_unpack(key[0], d, key[1], half, dst)
+            # send buffers are reused by the next pack: every stream waits for
+            # every receiver's copies first
+            copied = [torch.cuda.Event() for _ in range(n)]
+            for r in range(n):
+                copied[r].record(self.streams[r])
+            for r in range(n):
+                for q in range(n):
+                    if q != r:
+                        self.streams[r].wait_event(copied[q])
 
     def exchange(self, half):
+        if self.stream_ordered:
+            return self._exchange_streams(half)
         import torch
         for d in range(self.plan.dim):
             for e in self.engines:
@@ -214,4 +284,7 @@ class LoopbackWorld:
         self.exchange(half=1)
         dts = [e.stage_compute(2, dt)[0] for e in self.engines]
         self.exchange(half=0)
+        if self.stream_ordered:  # the half=0 exchange must land before the host reads state
+            for s in self.streams:
+                s.synchronize()
         return min(dts)

@@ -163,6 +163,15 @@ class GpuSolver:
     def halo_pack(self, gid, d, side, half, buf):
         self._check(self.L.pmhd_gpu_halo_pack(self.mesh, gid, d, side, int(half), C.c_void_p(buf.data_ptr())))
 
+    def set_async(self, on=True):
+        """Stream-ordered multi-rank mode (pmhd_gpu_set_async)."""
+        self._check(self.L.pmhd_gpu_set_async(self.mesh, int(on)))
+
+    def torch_stream(self):
+        """The context's stream as a torch.cuda.ExternalStream."""
+        import torch
+        return torch.cuda.ExternalStream(self.stream_handle, device=torch.device("cuda", self.device))
+
     def halo_unpack(self, gid, d, side, half, buf):
         self._check(self.L.pmhd_gpu_halo_unpack(self.mesh, gid, d, side, int(half), C.c_void_p(buf.data_ptr())))
 

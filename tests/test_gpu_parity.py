@@ -233,12 +233,14 @@ def test_kslab_pipeline_bitwise(gpu_available, slab, case, monkeypatch):
             assert np.array_equal(getattr(bo, f), getattr(bg, f)), (gid, f)
 
 
-@pytest.mark.parametrize("nranks", [2, 4])
-def test_multirank_halo_path_bitwise(gpu_available, nranks):
+@pytest.mark.parametrize("nranks,stream_ordered", [(2, False), (4, False), (2, True), (4, True)])
+def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered):
     """The multi-rank data path (stage_compute + local sweeps + halo pack /
     unpack kernels + transport) with nranks rank-engines on ONE GPU, stepped in
     lockstep by the host (no kernel waits on another), is bit-identical to the
-    oracle: the GPU side of SURVEY.md §8e."""
+    oracle: the GPU side of SURVEY.md §8e.  stream_ordered: the async ABI mode
+    with the hand-over ordered by events between the engines' streams (what
+    DistributedVL2 does with NCCL), i.e. no host synchronization in a stage."""
     from paper_1905_04341_b200.parallel import plan_for, LoopbackWorld
     kw = dict(nx1=32, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, x2max=0.5, x3max=0.5, wave_n1=1,
               wave_n2=1, wave_amp=1e-3)
@@ -247,8 +249,11 @@ def test_multirank_halo_path_bitwise(gpu_available, nranks):
     engines = [GpuSolver(cfg, parity=True, gids=plan.local_gids(r)) for r in range(nranks)]
     for e in engines:
         e.load_pgen(exchange=False)
-    world = LoopbackWorld(engines, plan)
+    world = LoopbackWorld(engines, plan, stream_ordered=stream_ordered)
     world.exchange(half=0)
+    if stream_ordered:
+        for s in world.streams:
+            s.synchronize()
     o = OracleSolver(cfg, workers=8)
     o.load_pgen()
     dt = o.new_dt()
