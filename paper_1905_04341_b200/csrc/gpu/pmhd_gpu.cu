@@ -347,7 +347,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   G.nb = int(m->gids.size());
   if (const char* kv = std::getenv("PMHD_KERNELS")) m->variant = (std::string(kv) == "split") ? 1 : 0;
   if (const char* sp = std::getenv("PMHD_SLAB_PLANES")) m->slab_planes = std::atoi(sp);
-  if (m->slab_planes > 0) m->slab_planes = std::max(8, (m->slab_planes / 8) * 8);  // tile multiple
+  if (m->slab_planes > 0) m->slab_planes = std::max(16, (m->slab_planes / 16) * 16);  // x3 tile multiple
   m->ph.gamma = desc->gamma;
   m->ph.gm1 = desc->gamma - 1.0;
   m->ph.igm1 = 1.0 / (desc->gamma - 1.0);

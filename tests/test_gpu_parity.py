@@ -209,7 +209,7 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
         assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
 
 
-@pytest.mark.parametrize("slab", [8, 16])
+@pytest.mark.parametrize("slab", [16, 32])
 @pytest.mark.parametrize("case", ["blast", "wave"])
 def test_kslab_pipeline_bitwise(gpu_available, slab, case, monkeypatch):
     """The two-stream k-slab pipeline (flux kernels of slab q+1 overlapping
@@ -220,7 +220,7 @@ def test_kslab_pipeline_bitwise(gpu_available, slab, case, monkeypatch):
                   x2min=-0.5, x2max=0.5, x3min=-1.0, x3max=1.0, pgen="blast", eos_mode="floor",
                   blast_r=0.2)
     else:
-        kw = dict(nx1=16, nx2=16, nx3=48, mb1=16, mb2=16, mb3=48, x3max=3.0, wave_n1=1, wave_n3=1,
+        kw = dict(nx1=16, nx2=16, nx3=64, mb1=16, mb2=16, mb3=64, x3max=4.0, wave_n1=1, wave_n3=1,
                   wave_amp=1e-3)
     cfg = RunConfig(**kw)
     o, g, _, (fo, fg), dts = run_pair(cfg, 3, parity=True)
