@@ -25,7 +25,10 @@ namespace pmhd_gpu {
 namespace {
 
 #ifndef PMHD_FLUX_T_FX
-#define PMHD_FLUX_T_FX 16  // x2 / x3 tiles: faces along i (x1 tiles: 32)
+#define PMHD_FLUX_T_FX 16  // x2 / x3 tiles: faces along i
+#endif
+#ifndef PMHD_FLUX_X1_FX
+#define PMHD_FLUX_X1_FX 32  // x1 tiles: faces along i
 #endif
 constexpr int NTHR = 128;
 #ifndef PMHD_FLUX_SMEMW
@@ -47,7 +50,7 @@ struct TileShape {
   // faces per tile: 32 x 8 for x1 (halo along i: 36 x 8 cells); 16 x 16 for
   // x2 / x3 (halo along the second axis: 16 x 19 cells, 1.19 cells per face
   // instead of 1.375 for 32 x 8, and 34 KB of shared memory instead of 39 KB)
-  static constexpr int FX = (DIR == 0) ? 32 : PMHD_FLUX_T_FX;  // faces along i
+  static constexpr int FX = (DIR == 0) ? PMHD_FLUX_X1_FX : PMHD_FLUX_T_FX;  // faces along i
   static constexpr int FS = 256 / FX;                          // faces along the 2nd axis
   static constexpr int NCOL = (DIR == 0) ? FX + 4 : FX;  // cells along i
   static constexpr int NROW = (DIR == 0) ? FS : FS + 3;  // cells along the 2nd axis
