@@ -25,7 +25,7 @@ constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0
 #define PMHD_UPDATE_MINB 5  // resident CTAs per SM the register budget targets (48 regs)
 #endif
 #ifndef PMHD_UPDATE_SEG
-#define PMHD_UPDATE_SEG 16  // k planes marched by one CTA
+#define PMHD_UPDATE_SEG 16  // max k planes marched by one CTA (shorter for small meshes)
 #endif
 
 // A CTA owns a 32 x 8 (i, j) column of cells and marches k through a segment
@@ -33,6 +33,7 @@ constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0
 // recomputed: the cell-centred E ring holds planes k and k+1 (one new plane
 // loaded per step), E1 / E2 at k+1/2 become the k-1/2 values of the next
 // step, and so does the new b3 face at k+1.
+template <int SEG>
 __global__ void __launch_bounds__(UTHR, PMHD_UPDATE_MINB)
 k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, DevRed* red,
                int want_dt, int kr0, int kr1) {
@@ -46,10 +47,10 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   __shared__ double redbuf[UTHR / 32];
 
   const bool d3 = (G.dim == 3);
-  const int nseg = (kr1 - kr0 + PMHD_UPDATE_SEG - 1) / PMHD_UPDATE_SEG;
+  const int nseg = (kr1 - kr0 + SEG - 1) / SEG;
   const int b = blockIdx.z / nseg;
-  const int kb = kr0 + (int)(blockIdx.z % nseg) * PMHD_UPDATE_SEG;
-  const int kend = min(kb + PMHD_UPDATE_SEG, kr1);
+  const int kb = kr0 + (int)(blockIdx.z % nseg) * SEG;
+  const int kend = min(kb + SEG, kr1);
   const int i0 = G.is + blockIdx.x * UX, j0 = G.js + blockIdx.y * UY;
   const int nx = min(UX, G.ie - i0), ny = min(UY, G.je - j0);
   const DevBlock& B = blks[b];
@@ -244,9 +245,21 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
 
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                          DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s) {
-  const int nseg = (kr1 - kr0 + PMHD_UPDATE_SEG - 1) / PMHD_UPDATE_SEG;
+  // segment length: PMHD_UPDATE_SEG planes, or 4 / 1 when the mesh is too
+  // small to fill ~2 waves of 148 SMs x 5 CTAs otherwise
+  const int tiles = ((G.ie - G.is + UX - 1) / UX) * ((G.je - G.js + UY - 1) / UY) * G.nb;
+  const int nk = kr1 - kr0;
+  const int want = (2 * 148 * PMHD_UPDATE_MINB + tiles - 1) / tiles;  // segments per column
+  const int fit = (nk + want - 1) / want;                              // planes per segment
+  const int seg = (fit >= PMHD_UPDATE_SEG) ? PMHD_UPDATE_SEG : (fit >= 4 ? 4 : 1);
+  const int nseg = (nk + seg - 1) / seg;
   const dim3 grid((G.ie - G.is + UX - 1) / UX, (G.je - G.js + UY - 1) / UY, nseg * G.nb);
-  k_update_fused<<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);
+  if (seg == PMHD_UPDATE_SEG)
+    k_update_fused<PMHD_UPDATE_SEG><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);
+  else if (seg == 4)
+    k_update_fused<4><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);
+  else
+    k_update_fused<1><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);
 }
 
 }  // namespace pmhd_gpu
