@@ -169,7 +169,6 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       double* const q = &sw[n][threadIdx.x];
 #pragma unroll
       for (int p = 0; p < TS::PER; ++p) {
-        lo[p] = hi[p] = 0.0;
         if (vmask & (1u << p)) {
           const double q0 = q[p * NTHR];
           const double dq = plm_slope(q[p * NTHR - TS::DC], q0, q[p * NTHR + TS::DC], ph.limiter);
