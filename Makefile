@@ -22,9 +22,9 @@ all: host gpu cli oracle testlib
 host: $(LIB)/libpmhd_host.so
 gpu: $(LIB)/libpmhd_gpu.so $(LIB)/libpmhd_gpu_parity.so
 
-$(LIB)/libpmhd_host.so: $(PKG)/csrc/host/pmhd_host.cpp $(PKG)/csrc/host/snapshot.cpp include/pmhd_host.h include/pmhd_gpu.h
+$(LIB)/libpmhd_host.so: $(PKG)/csrc/host/pmhd_host.cpp $(PKG)/csrc/host/snapshot.cpp $(PKG)/csrc/host/perf_model.cpp include/pmhd_host.h include/pmhd_gpu.h
 	@mkdir -p $(LIB)
-	$(HOSTCXX) $(HOSTFLAGS) -shared -o $@ $(PKG)/csrc/host/pmhd_host.cpp $(PKG)/csrc/host/snapshot.cpp
+	$(HOSTCXX) $(HOSTFLAGS) -shared -o $@ $(PKG)/csrc/host/pmhd_host.cpp $(PKG)/csrc/host/snapshot.cpp $(PKG)/csrc/host/perf_model.cpp
 
 $(LIB)/libpmhd_gpu.so: $(GPU_DEPS)
 	@mkdir -p $(LIB)

@@ -313,8 +313,8 @@ def run_ours(args):
         dt = step(dt)
     rt = g.region_times(reset=True)
     g.set_profiling(False)
-    kern_ms = (rt["c2p_ms"] + rt["riemann_ms"] + rt["ct_emf_ms"] + rt["integrate_ms"] +
-               rt["boundary_ms"]) / nprof
+    kern_ms = (rt["c2p_ms"] + rt["reconstruct_ms"] + rt["riemann_ms"] + rt["ct_emf_ms"] +
+               rt["integrate_ms"] + rt["boundary_ms"]) / nprof
     F_alg, F_flux, F_src = falg()
     fp64_pk, fp64_src = fp64_peak()
     hbm_pk, hbm_src = hbm_peak()
@@ -322,23 +322,25 @@ def run_ours(args):
     ach_gbs = B_ALG * cells_rank / (cycle_ms_kernels * 1e-3) / 1e9
     ach_tf = F_alg * cells_rank / (cycle_ms_kernels * 1e-3) / 1e12
     shares = {k: rt[k] / max(1e-9, kern_ms * nprof) for k in
-              ("c2p_ms", "riemann_ms", "ct_emf_ms", "integrate_ms", "boundary_ms")}
+              ("c2p_ms", "reconstruct_ms", "riemann_ms", "ct_emf_ms", "integrate_ms", "boundary_ms")}
     # Dominant kernel: the fused flux kernel (c2p + PLM + Riemann), 2*dim
     # launches per cycle, timed with CUDA events on the ABI stream (region
     # "riemann").  It is FP64-pipe bound (no dense contraction, < 30 % of HBM
     # bandwidth in ncu), so its roofline is the measured DFMA peak.
     dim = cfg.dim
     n_flux = 2 * dim
-    flux_ms = rt["riemann_ms"] / nprof / n_flux            # average launch duration
+    # average launch duration (the fused kernel's time is split over the c2p /
+    # reconstruct / riemann regions by its phase shares; their sum is the kernel)
+    flux_ms = (rt["c2p_ms"] + rt["reconstruct_ms"] + rt["riemann_ms"]) / nprof / n_flux
     flux_flops = F_flux * cells_rank / n_flux              # algorithmic flops per launch
     flux_tf = flux_flops / (flux_ms * 1e-3) / 1e12
     tr = ncu_traffic() if args.size == 256 and dim == 3 else None
-    upd_ms = rt["integrate_ms"] / nprof / 2
+    upd_ms = (rt["ct_emf_ms"] + rt["integrate_ms"]) / nprof / 2  # update kernel = ct_emf + integrate regions
     roofline = {
         "bound": "fp64", "achieved": flux_tf, "peak": fp64_pk, "unit": "TFLOP/s",
         "frac": flux_tf / fp64_pk,
         "traffic": tr["flux_bytes_per_launch"] if tr else None,
-        "kernel": f"k_flux_fused (dominant: {shares['riemann_ms']:.0%} of the cycle; {n_flux} launches/cycle, "
+        "kernel": f"k_flux_fused (dominant: {shares['c2p_ms'] + shares['reconstruct_ms'] + shares['riemann_ms']:.0%} of the cycle; {n_flux} launches/cycle, "
                   f"avg {flux_ms:.3f} ms; F_alg(flux region) = {F_flux:.1f} flop/cell-update / {n_flux} launches)",
         "peak_source": fp64_src,
         "note": "FP64 CUDA-core bound, neither HBM nor tensor cores: bound='fp64' against the measured DFMA peak",
@@ -356,6 +358,7 @@ def run_ours(args):
         min(hbm_pk * 1e9 / B_ALG, fp64_pk * 1e12 / F_alg),
         "region_share": shares,
         "dominant_region": max(shares, key=shares.get),
+        "region_split": "fused kernels: event time per kernel split by in-kernel clock64 phase shares",
     }
 
     # ---- e2e through the public API with pinned host buffers ----

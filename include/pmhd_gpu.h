@@ -102,6 +102,10 @@ typedef struct pmhd_region_times {
   double c2p_ms, riemann_ms, ct_emf_ms, integrate_ms, boundary_ms, dt_ms;
   long long calls;           /* profiled stages                               */
   long long kernel_launches; /* kernels this library launched (always counted) */
+  /* reconstruction ("reconstruct").  The fused kernels' event
+   * times are split into c2p / reconstruct / riemann and ct_emf / integrate
+   * by the SM-cycle shares of their phases (clock64 at the kernel barriers). */
+  double reconstruct_ms;
 } pmhd_region_times;
 
 typedef struct pmhd_ctx pmhd_ctx;

@@ -109,6 +109,39 @@ int pmhd_host_snapshot_write(const char* path, const pmhd_run_config* cfg, doubl
 int pmhd_host_snapshot_read(const char* path, const pmhd_run_config* cfg, double* t, double* const* u,
                             double* const* b1f, double* const* b2f, double* const* b3f);
 
+/* ---- perf_model: roofline (Eq. 1), architectural
+ * efficiency (Eq. 2), performance-portability metric (Eq. 3) over platform
+ * records (Table 2 schema).  Pure functions; bandwidths in B/s, peaks in
+ * FLOP/s. */
+#define PMHD_PERF_MAX_SPACES 8
+typedef struct pmhd_platform {
+  char id[32];
+  double t_peak;                                /* FLOP/s (double precision) */
+  int nspace;
+  char space[PMHD_PERF_MAX_SPACES][16];         /* memory-space labels ("dram", "l2", ...) */
+  double bw[PMHD_PERF_MAX_SPACES];              /* B/s per space */
+} pmhd_platform;
+
+/* load_platform_table: CSV text with header `id,t_peak_gflops,bw_<space>_gbs...`
+ * (GFLOP/s, GB/s).  Missing / non-numeric / non-positive field ->
+ * PMHD_ERR_INPUT with the 1-based line in *err_line.  Empty text -> 0 rows. */
+int pmhd_perf_load_platforms(const char* text, pmhd_platform* out, int max_rows, int* n_rows,
+                             int* err_line, char* err, int errlen);
+/* The same schema back (round trip of load); returns the bytes needed. */
+int pmhd_perf_format_platforms(const pmhd_platform* p, int n, char* buf, int buflen);
+/* roofline_cap (Eq. 1) for one kernel intensity set: P_max = min over the
+ * given spaces of min(T_peak, B(space) * I(space)); *binding = -1 when the
+ * compute peak binds, else the index of the binding space.  Unknown space ->
+ * PMHD_ERR_INPUT. */
+int pmhd_perf_roofline_cap(const pmhd_platform* p, const char* const* spaces, const double* intensity,
+                           int n, double* cap, int* binding);
+/* arch_efficiency (Eq. 2): e = eps / cap; *flag = 1 when e > 1 (reported, not
+ * clamped).  cap <= 0 -> PMHD_ERR_INPUT. */
+int pmhd_perf_arch_efficiency(double eps, double cap, double* e, int* flag);
+/* pp_metric (Eq. 3): |H| / sum 1/e over the platforms, 0 if any platform is
+ * unsupported (supported[i] == 0); a supported e <= 0 -> PMHD_ERR_INPUT. */
+int pmhd_perf_pp_metric(const double* e, const int* supported, int n, double* P);
+
 #ifdef __cplusplus
 }
 #endif

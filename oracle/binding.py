@@ -127,10 +127,13 @@ def flops_reset():
     lib().oracle_flops_reset()
 
 
+REGIONS = ("c2p", "reconstruct", "riemann", "ct_emf", "integrate")
+
+
 def region_flops():
-    """[flux region (c2p + reconstruction + Riemann), EMF + CT + update]
-    flops tallied by counting meshes since the last flops_reset()."""
-    out = np.zeros(2)
+    """Flops per region (REGIONS order) tallied by counting meshes since the
+    last flops_reset()."""
+    out = np.zeros(5)
     lib().oracle_region_flops(out.ctypes.data_as(_dp))
     return out
 

@@ -314,12 +314,11 @@ void oracle_flops(double out[4]) {
 }
 void oracle_flops_reset(void) {
   oracle::g_tally.reset();
-  oracle::g_region[0] = oracle::g_region[1] = 0.0;
+  for (double& r : oracle::g_region) r = 0.0;
 }
-// out[0] = flux region (c2p + PLM + Riemann), out[1] = EMF + CT + update.
-void oracle_region_flops(double out[2]) {
-  out[0] = oracle::g_region[0];
-  out[1] = oracle::g_region[1];
+// out[0..4] = c2p, reconstruct, riemann, ct_emf, integrate (counting.hpp).
+void oracle_region_flops(double out[5]) {
+  for (int q = 0; q < 5; ++q) out[q] = oracle::g_region[q];
 }
 
 //---------------------------------------------------------------- pointwise ops

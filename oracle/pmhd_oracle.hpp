@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -713,6 +714,8 @@ class Mesh {
     const int vars[7] = {IDN, iv[0], iv[1], iv[2], IPR, ib[0], ib[1]};
     par3(fb, [&](int k, int j, int i) {
       R wl[7], wr[7];
+      constexpr bool counting = std::is_same<R, Counting>::value;
+      const double r0 = counting ? g_tally.total() : 0.0;
       for (int n = 0; n < 7; ++n) {
         const Field<R>& q = B.w[vars[n]];
         const R qm1 = q(k - dk, j - dj, i - di);  // cell on the low side
@@ -728,7 +731,12 @@ class Mesh {
         }
       }
       R out[8];
+      const double r1 = counting ? g_tally.total() : 0.0;
       if (face_solve(wl, wr, bn(k, j, i), ph, c1024, out)) fallbacks.fetch_add(1);
+      if (counting) {  // counting meshes run one worker
+        g_region[1] += r1 - r0;
+        g_region[2] += g_tally.total() - r1;
+      }
       B.fx[dir][IDN](k, j, i) = out[0];  // un-rotate momentum fluxes
       B.fx[dir][iv[0]](k, j, i) = out[1];
       B.fx[dir][iv[1]](k, j, i) = out[2];
@@ -1011,13 +1019,16 @@ class Mesh {
       const State<R>& in = (s == 1) ? B.A : B.B;
       const double f0 = g_tally.total();
       c2p_all(B, in, bad);
-      for (int dir = 0; dir < g.dim; ++dir) fluxes(B, in, dir, s == 2, dt);
       const double f1 = g_tally.total();
+      for (int dir = 0; dir < g.dim; ++dir) fluxes(B, in, dir, s == 2, dt);  // splits [1] / [2]
+      const double f2 = g_tally.total();
       emfs(B);
+      const double f3 = g_tally.total();
       State<R>& out = (s == 1) ? B.B : B.A;
       update(B, B.A, out, (s == 1) ? 0.5 : 1.0, dt, bad, nfloor);
-      g_region[0] += f1 - f0;  // (tally only moves in counting meshes)
-      g_region[1] += g_tally.total() - f1;
+      g_region[0] += f1 - f0;  // (the tally only moves in counting meshes)
+      g_region[3] += f3 - f2;
+      g_region[4] += g_tally.total() - f3;
     }
     if (do_exchange) exchange(s == 1);
   }

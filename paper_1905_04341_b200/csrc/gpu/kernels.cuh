@@ -49,6 +49,10 @@ struct DevRed {
   unsigned long long floor_count;
   unsigned long long divb_bits;   // max |div B| as bits
   unsigned long long fallback_count;  // Roe -> HLLE fallbacks
+  // profiling only (KPhys::prof): SM cycles summed over CTAs per kernel phase
+  // -- flux: [0] load + cons_to_prim, [1] reconstruct, [2] Riemann;
+  // update: [3] Ec + corner EMFs, [4] CT + conserved update + c2p + dt
+  unsigned long long phase[5];
 };
 
 // Stage coefficients c_d = beta*dt/dx_d, computed on the host with the same

@@ -66,7 +66,7 @@ __device__ __forceinline__ int rot_var(int n) {
   return V[DIR][n];
 }
 
-template <int DIR, int RS>
+template <int DIR, int RS, bool PROF>
 __global__ void __launch_bounds__(NTHR, FluxMinB<RS>::value)
 k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024,
              int stage, DevRed* red, int write_ec, int f_i0, int f_i1, int f_s0, int f_s1, int f_t0,
@@ -74,6 +74,8 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   using TS = TileShape<DIR>;
   __shared__ double sw[7][TS::NCELL];  // primitives; after phase 2: q - dq/2 (low-face value)
   __shared__ double sp[7][TS::NCELL];  // after phase 2: q + dq/2 (high-face value)
+  __shared__ long long tph[3];          // profiling: phase start clocks (thread 0)
+  if (PROF && threadIdx.x == 0) tph[0] = clock64();
 
   const int nt = f_t1 - f_t0;
   const int b = blockIdx.z / nt;
@@ -150,6 +152,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     for (int n = 0; n < 7; ++n) sw[n][c] = w[rot_var<DIR>(n)];
   }
   __syncthreads();
+  if (PROF && threadIdx.x == 0) tph[1] = clock64();
 
   // ---- phase 2: per-cell reconstruction, one variable at a time ------------
   if (plm) {
@@ -187,6 +190,8 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     }
     __syncthreads();
   }
+
+  if (PROF && threadIdx.x == 0) tph[2] = clock64();
 
   // ---- phase 3: two faces per thread ---------------------------------------
   const int fc = threadIdx.x % FX;
@@ -230,6 +235,15 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     F[6][id] = out[6];
     F[7][id] = out[7];
   }
+  if (PROF) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long t3 = clock64();
+      atomicAdd(&red[stage].phase[0], (unsigned long long)(tph[1] - tph[0]));
+      atomicAdd(&red[stage].phase[1], (unsigned long long)(tph[2] - tph[1]));
+      atomicAdd(&red[stage].phase[2], (unsigned long long)(t3 - tph[2]));
+    }
+  }
 }
 
 }  // namespace
@@ -266,9 +280,15 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
     }
   }
   const dim3 grid((i1 - i0 + FX - 1) / FX, ty1 - ty0, (nt1 - nt0) * G.nb);
-#define PMHD_FLUX_LAUNCH(D, R)                                                                    \
-  k_flux_fused<D, R><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red, write_ec, i0, \
-                                           i1, ns0, ns1, nt0, nt1, ty0)
+#define PMHD_FLUX_LAUNCH(D, R)                                                                      \
+  do {                                                                                              \
+    if (ph.prof)                                                                                    \
+      k_flux_fused<D, R, true><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red,      \
+                                                     write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0);    \
+    else                                                                                            \
+      k_flux_fused<D, R, false><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red,     \
+                                                      write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0);   \
+  } while (0)
 #define PMHD_FLUX_DIRS(R)                          \
   do {                                             \
     if (dir == 0) PMHD_FLUX_LAUNCH(0, R);          \

@@ -33,7 +33,7 @@ constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0
 // recomputed: the cell-centred E ring holds planes k and k+1 (one new plane
 // loaded per step), E1 / E2 at k+1/2 become the k-1/2 values of the next
 // step, and so does the new b3 face at k+1.
-template <int SEG>
+template <int SEG, bool PROF>
 __global__ void __launch_bounds__(UTHR, PMHD_UPDATE_MINB)
 k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, DevRed* red,
                int want_dt, int kr0, int kr1) {
@@ -45,6 +45,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   __shared__ double b2s[UY + 1][UX];
   __shared__ double b3s[2][UY][UX];        // new b3 at faces k / k+1, slot by parity
   __shared__ double redbuf[UTHR / 32];
+  __shared__ long long tph[3];  // profiling (thread 0): mark, EMF cycles, update cycles
+  if (PROF && threadIdx.x == 0) { tph[0] = clock64(); tph[1] = tph[2] = 0; }
 
   const bool d3 = (G.dim == 3);
   const int nseg = (kr1 - kr0 + SEG - 1) / SEG;
@@ -137,6 +139,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   double tmin = 1.0e300;
   for (int k = kb; k < kend; ++k) {
     const int lo = k & 1, hi = lo ^ 1;  // slots of k - 1/2 and k + 1/2
+    if (PROF && tid == 0 && k > kb) { const long long t = clock64(); tph[2] += t - tph[0]; tph[0] = t; }
     // ---- A: the next Ec plane (slot of k-1, no longer needed) --------------
     if (d3) load_ec(k + 1);
     __syncthreads();
@@ -154,6 +157,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
     }
     edge_emfs(k + 1, hi);
     __syncthreads();
+    if (PROF && tid == 0) { const long long t = clock64(); tph[1] += t - tph[0]; tph[0] = t; }
     // ---- C: constrained-transport face update -------------------------------
     for (int q = tid; q < UY * (UX + 1); q += UTHR) {  // b1f, faces i0 .. i0+nx
       const int c = q % (UX + 1), r = q / (UX + 1);
@@ -229,6 +233,14 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
       }
     }
   }
+  if (PROF) {
+    __syncthreads();
+    if (tid == 0) {
+      tph[2] += clock64() - tph[0];
+      atomicAdd(&red[ks.stage].phase[3], (unsigned long long)tph[1]);
+      atomicAdd(&red[ks.stage].phase[4], (unsigned long long)tph[2]);
+    }
+  }
   if (want_dt) {
     for (int o = 16; o > 0; o >>= 1) tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
     if ((tid & 31) == 0) redbuf[tid >> 5] = tmin;
@@ -254,12 +266,17 @@ void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, 
   const int seg = (fit >= PMHD_UPDATE_SEG) ? PMHD_UPDATE_SEG : (fit >= 4 ? 4 : 1);
   const int nseg = (nk + seg - 1) / seg;
   const dim3 grid((G.ie - G.is + UX - 1) / UX, (G.je - G.js + UY - 1) / UY, nseg * G.nb);
-  if (seg == PMHD_UPDATE_SEG)
-    k_update_fused<PMHD_UPDATE_SEG><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);
-  else if (seg == 4)
-    k_update_fused<4><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);
-  else
-    k_update_fused<1><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);
+#define PMHD_UPDATE_LAUNCH(SG)                                                                    \
+  do {                                                                                            \
+    if (ph.prof)                                                                                  \
+      k_update_fused<SG, true><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);   \
+    else                                                                                          \
+      k_update_fused<SG, false><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);  \
+  } while (0)
+  if (seg == PMHD_UPDATE_SEG) PMHD_UPDATE_LAUNCH(PMHD_UPDATE_SEG);
+  else if (seg == 4) PMHD_UPDATE_LAUNCH(4);
+  else PMHD_UPDATE_LAUNCH(1);
+#undef PMHD_UPDATE_LAUNCH
 }
 
 }  // namespace pmhd_gpu

@@ -117,6 +117,7 @@ int reset_red(pmhd_mesh* m) {
     m->hred[s].floor_count = 0;
     m->hred[s].divb_bits = 0;
     m->hred[s].fallback_count = 0;
+    for (int q = 0; q < 5; ++q) m->hred[s].phase[q] = 0;
   }
   CK(cudaMemcpyAsync(m->dred, m->hred, 3 * sizeof(DevRed), cudaMemcpyHostToDevice, ctx->stream));
   return PMHD_OK;
@@ -214,10 +215,30 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true) {
     CK(cudaEventSynchronize(m->ev[5]));
     float t[5];
     for (int q = 0; q < 5; ++q) cudaEventElapsedTime(&t[q], m->ev[q], m->ev[q + 1]);
-    m->times.c2p_ms += t[0];
-    m->times.riemann_ms += t[1];
-    m->times.ct_emf_ms += t[2];
-    m->times.integrate_ms += t[3];
+    double c2p = t[0], rec_ms = 0.0, rie = t[1], emf = t[2], integ = t[3];
+    if (m->variant == 0) {
+      // fused kernels: split each kernel's event time by the SM-cycle shares
+      // of its phases (clock64 at the kernels' barriers, summed over CTAs)
+      int rc = fetch_red(m);
+      if (rc) return rc;
+      const unsigned long long* ph = m->hred[s].phase;
+      const double pf = double(ph[0]) + double(ph[1]) + double(ph[2]);
+      const double pu = double(ph[3]) + double(ph[4]);
+      if (pf > 0.0) {
+        c2p += t[1] * double(ph[0]) / pf;
+        rec_ms = t[1] * double(ph[1]) / pf;
+        rie = t[1] * double(ph[2]) / pf;
+      }
+      if (pu > 0.0) {
+        emf += t[3] * double(ph[3]) / pu;
+        integ = t[3] * double(ph[4]) / pu;
+      }
+    }
+    m->times.c2p_ms += c2p;
+    m->times.reconstruct_ms += rec_ms;
+    m->times.riemann_ms += rie;
+    m->times.ct_emf_ms += emf;
+    m->times.integrate_ms += integ;
     m->times.boundary_ms += t[4];
     m->times.calls += 1;
   }
@@ -357,6 +378,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   m->ph.limiter = desc->limiter;
   m->ph.eos = desc->eos_mode;
   m->ph.emf = desc->emf_mode;
+  m->ph.prof = 0;
 
   // one slab: 59 arrays per block, each (n3+1)*sy doubles plus a 64-double guard
   const size_t arr = size_t(G.n3 + 1) * size_t(G.sy) + 64;
@@ -738,6 +760,7 @@ int pmhd_gpu_halo_unpack(pmhd_mesh* m, int gid, int dir, int side, int half, con
 int pmhd_gpu_set_profiling(pmhd_mesh* m, int on) {
   if (!m) return PMHD_ERR_INPUT;
   m->prof = on != 0;
+  m->ph.prof = m->prof ? 1 : 0;
   return PMHD_OK;
 }
 

@@ -5,6 +5,12 @@
 //   pmhd run   --config <file> [--out <dir>] [--device <d>] [--restart <snapshot>]
 //                                                             (cmd_run)
 //   pmhd bench --config <file> [--cycles <n>] [--warmup <w>]  (cmd_bench)
+//   pmhd report --config <file> [--cycles <n>] [--warmup <w>] [--falg <csv>] [--out <dir>]
+//        Fig. 3 analogue (with_region report): profile.csv =
+//        region, calls, time_s, time_normalized, flops, bytes, intensity
+//   pmhd roofline --config <file> --platform <csv> [--platform-id <id>] [--falg <csv>] ...
+//        cmd_roofline: Eq. 1-3 reports roofline.csv and
+//        portability.csv (perf_model)
 //
 // run: evolves to tlim (default: one wave period) or nlim cycles, prints
 // cycles / wall time / cell-updates per second, writes errors.csv (linear
@@ -28,14 +34,16 @@
 namespace {
 
 struct Args {
-  std::string cmd, config, out = ".", restart;
+  std::string cmd, config, out = ".", restart, falg = "profiles/falg_regions.csv", platform,
+      platform_id = "b200";
   int device = 0, cycles = 10, warmup = 2;
 };
 
 int usage() {
   std::fprintf(stderr,
-               "usage: pmhd run|bench --config <file> [--out <dir>] [--device <d>] [--cycles <n>] "
-               "[--warmup <w>] [--restart <snapshot>]\n");
+               "usage: pmhd run|bench|report|roofline --config <file> [--out <dir>] [--device <d>] "
+               "[--cycles <n>] [--warmup <w>] [--restart <snapshot>] [--falg <csv>] "
+               "[--platform <csv>] [--platform-id <id>]\n");
   return 2;
 }
 
@@ -63,6 +71,142 @@ struct Blocks {
   }
 };
 
+// Algorithmic flops per cell-update by region (tools/count_falg.py: the CPU
+// oracle on the CountingScalar restatement, one cycle of the bench config).
+bool load_falg(const std::string& path, std::vector<std::pair<std::string, double>>* rows) {
+  std::ifstream f(path);
+  if (!f) return false;
+  std::string line;
+  std::getline(f, line);  // header region,flops_per_cell_update
+  while (std::getline(f, line)) {
+    const size_t c = line.find(',');
+    if (c == std::string::npos) continue;
+    rows->push_back({line.substr(0, c), std::atof(line.c_str() + c + 1)});
+  }
+  return !rows->empty();
+}
+
+// Streaming-byte model of THIS implementation's kernels per cell-update
+// (8 B per array element read or written once per kernel, SPEC.md:330's
+// convention applied to the fused kernels; 3D, both stages): the flux kernels
+// read the 8 state arrays over their stencil tiles (~1.15 cells per face) and
+// write 8 face arrays per direction (+3 cell-E arrays in the last direction);
+// the update kernel reads 9 EMF inputs + 3 cell-E (ct_emf) and 15 fluxes + 8
+// base state, writing 8 (integrate).  Loads are attributed to c2p and stores
+// to riemann (reconstruct works in shared memory).
+double region_bytes(const std::string& r, int dim) {
+  const double nd = dim;
+  if (r == "c2p") return 2.0 * nd * 8.0 * 1.15 * 8.0;
+  if (r == "riemann") return 2.0 * (nd * 8.0 + 3.0) * 8.0;
+  if (r == "ct_emf") return 2.0 * (3.0 * nd + 3.0) * 8.0;
+  if (r == "integrate") return 2.0 * (5.0 * nd + 16.0) * 8.0;
+  return 0.0;
+}
+
+int cmd_report(const Args& a, const pmhd_run_config& cfg, pmhd_mesh* mesh, long long cells, double* t,
+               double* dt) {
+  std::vector<std::pair<std::string, double>> falg;
+  if (!load_falg(a.falg, &falg)) {
+    std::fprintf(stderr, "no flop table %s (python tools/count_falg.py writes it)\n", a.falg.c_str());
+    return 1;
+  }
+  pmhd_status st;
+  int done = 0;
+  if (pmhd_gpu_run(mesh, a.warmup, -1.0, t, dt, &done, &st)) return 1;
+  // timed pass (no profiling: no region synchronisation) for epsilon
+  auto t0 = std::chrono::steady_clock::now();
+  if (pmhd_gpu_run(mesh, a.cycles, -1.0, t, dt, &done, &st)) return 1;
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  // profiled pass for the region breakdown
+  pmhd_region_times rt;
+  pmhd_gpu_region_times(mesh, nullptr, 1);
+  pmhd_gpu_set_profiling(mesh, 1);
+  auto tp = std::chrono::steady_clock::now();
+  if (pmhd_gpu_run(mesh, a.cycles, -1.0, t, dt, &done, &st)) return 1;
+  const double wall_prof = std::chrono::duration<double>(std::chrono::steady_clock::now() - tp).count();
+  pmhd_gpu_set_profiling(mesh, 0);
+  pmhd_gpu_region_times(mesh, &rt, 1);
+  const int ncyc = done;
+  const double upd = double(cells) * ncyc;
+  struct Reg { std::string name; double ms; };
+  const std::vector<Reg> regs = {{"c2p", rt.c2p_ms},         {"reconstruct", rt.reconstruct_ms},
+                                 {"riemann", rt.riemann_ms}, {"ct_emf", rt.ct_emf_ms},
+                                 {"integrate", rt.integrate_ms}, {"boundary", rt.boundary_ms}};
+  double fl_tot = 0.0;
+  for (auto& f : falg) fl_tot += f.second;
+  mkdir(a.out.c_str(), 0755);
+  const int dim = cfg.mesh.nx[2] > 1 ? 3 : 2;
+  if (a.cmd == "report") {
+    const double rie = rt.riemann_ms > 0 ? rt.riemann_ms : 1.0;
+    FILE* f = std::fopen((a.out + "/profile.csv").c_str(), "w");
+    std::fprintf(f, "region,calls,time_s,time_normalized,flops,bytes,intensity\n");
+    double tot_ms = 0.0;
+    for (auto& r : regs) {
+      double fpc = 0.0;
+      for (auto& q : falg) if (q.first == r.name || (r.name == "integrate" && q.first == "dt")) fpc += q.second;
+      const double flops = fpc * upd, bytes = region_bytes(r.name, dim) * upd;
+      std::fprintf(f, "%s,%lld,%.9g,%.6g,%.6g,%.6g,%.6g\n", r.name.c_str(), (long long)rt.calls,
+                   r.ms * 1e-3, r.ms / rie, flops, bytes, bytes > 0 ? flops / bytes : 0.0);
+      tot_ms += r.ms;
+    }
+    std::fclose(f);
+    // SPEC.md:546 (acceptance 11): named regions partition >= 90 % of a cycle
+    std::printf("profile.csv: %d cycles; regions cover %.1f %% of the profiled wall time (%.3f of %.3f ms); "
+                "unprofiled pass %.4e cell-updates/s\n",
+                ncyc, 100.0 * tot_ms / (wall_prof * 1e3), tot_ms, wall_prof * 1e3, upd / wall);
+    return 0;
+  }
+  // cmd_roofline: epsilon from the timed pass, intensity from F_alg / B_alg
+  std::ifstream pf(a.platform);
+  std::stringstream ss;
+  ss << pf.rdbuf();
+  pmhd_platform plats[16];
+  int np = 0, line = 0;
+  char err[256];
+  if (!pf || pmhd_perf_load_platforms(ss.str().c_str(), plats, 16, &np, &line, err, sizeof(err))) {
+    std::fprintf(stderr, "platform file %s: line %d: %s\n", a.platform.c_str(), line, err);
+    return 1;
+  }
+  int host = -1;
+  for (int i = 0; i < np; ++i) if (a.platform_id == plats[i].id) host = i;
+  if (host < 0) {
+    std::fprintf(stderr, "no platform record '%s' in %s\n", a.platform_id.c_str(), a.platform.c_str());
+    return 1;
+  }
+  const double b_alg = 320.0;  // compulsory bytes per cell-update
+  const double eps = fl_tot * upd / wall;
+  const double I = fl_tot / b_alg;
+  const char* sp = "dram";
+  double cap = 0.0, e = 0.0;
+  int bind = 0, flag = 0;
+  if (pmhd_perf_roofline_cap(&plats[host], &sp, &I, 1, &cap, &bind) ||
+      pmhd_perf_arch_efficiency(eps, cap, &e, &flag)) {
+    std::fprintf(stderr, "platform '%s' has no dram bandwidth\n", a.platform_id.c_str());
+    return 1;
+  }
+  FILE* f = std::fopen((a.out + "/portability.csv").c_str(), "w");
+  std::fprintf(f, "platform,space,epsilon_gflops,cap_gflops,efficiency\n");
+  std::fprintf(f, "%s,%s,%.6f,%.6f,%.6f\n", plats[host].id, sp, eps / 1e9, cap / 1e9, e);
+  double P = 0.0;
+  pmhd_perf_pp_metric(&e, nullptr, 1, &P);
+  std::fprintf(f, "pp_metric_%s,%.6f\n", sp, P);
+  std::fclose(f);
+  f = std::fopen((a.out + "/roofline.csv").c_str(), "w");  // Fig. 4-style sample points
+  std::fprintf(f, "series,space,intensity,gflops\n");
+  for (int q = 0; q <= 48; ++q) {
+    const double x = std::pow(2.0, -8.0 + q * 0.5);
+    double c;
+    int b;
+    pmhd_perf_roofline_cap(&plats[host], &sp, &x, 1, &c, &b);
+    std::fprintf(f, "ceiling,%s,%.6g,%.6f\n", sp, x, c / 1e9);
+  }
+  std::fprintf(f, "achieved,%s,%.6g,%.6f\n", sp, I, eps / 1e9);
+  std::fclose(f);
+  std::printf("roofline: eps %.1f GFLOP/s at I = %.3f flop/B, cap %.1f GFLOP/s (%s-bound), e = %.4f%s\n",
+              eps / 1e9, I, cap / 1e9, bind < 0 ? "compute" : sp, e, flag ? " (>1: model inconsistency)" : "");
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -78,9 +222,14 @@ int main(int argc, char** argv) {
     else if (s == "--device") a.device = std::atoi(next().c_str());
     else if (s == "--cycles") a.cycles = std::atoi(next().c_str());
     else if (s == "--warmup") a.warmup = std::atoi(next().c_str());
+    else if (s == "--falg") a.falg = next();
+    else if (s == "--platform") a.platform = next();
+    else if (s == "--platform-id") a.platform_id = next();
     else return usage();
   }
-  if ((a.cmd != "run" && a.cmd != "bench") || a.config.empty()) return usage();
+  if ((a.cmd != "run" && a.cmd != "bench" && a.cmd != "report" && a.cmd != "roofline") || a.config.empty())
+    return usage();
+  if (a.cmd == "roofline" && a.platform.empty()) return usage();
 
   pmhd_run_config cfg;
   pmhd_host_config_defaults(&cfg);
@@ -144,6 +293,8 @@ int main(int argc, char** argv) {
                 pmhd_gpu_build_info(), done, wall, double(cells) * done / wall);
     return 0;
   }
+
+  if (a.cmd == "report" || a.cmd == "roofline") return cmd_report(a, cfg, mesh, cells, &t, &dt);
 
   // cmd_run
   const double tlim = pmhd_host_default_tlim(&cfg);

@@ -77,6 +77,7 @@ class RegionTimes(C.Structure):
         ("dt_ms", C.c_double),
         ("calls", C.c_longlong),
         ("kernel_launches", C.c_longlong),
+        ("reconstruct_ms", C.c_double),
     ]
 
 
@@ -103,6 +104,16 @@ class RunConfigC(C.Structure):
         ("tlim", C.c_double),
         ("workers", C.c_int),
         ("gpus", C.c_int),
+    ]
+
+
+class PlatformC(C.Structure):
+    _fields_ = [
+        ("id", C.c_char * 32),
+        ("t_peak", C.c_double),
+        ("nspace", C.c_int),
+        ("space", (C.c_char * 16) * 8),
+        ("bw", C.c_double * 8),
     ]
 
 
@@ -141,6 +152,12 @@ def host_lib() -> C.CDLL:
         _pp = _P(_dp)
         L.pmhd_host_snapshot_write.argtypes = [C.c_char_p, _P(RunConfigC), C.c_double, _pp, _pp, _pp, _pp]
         L.pmhd_host_snapshot_read.argtypes = [C.c_char_p, _P(RunConfigC), _dp, _pp, _pp, _pp, _pp]
+        L.pmhd_perf_load_platforms.argtypes = [C.c_char_p, _P(PlatformC), C.c_int, _ip, _ip, C.c_char_p,
+                                               C.c_int]
+        L.pmhd_perf_format_platforms.argtypes = [_P(PlatformC), C.c_int, C.c_char_p, C.c_int]
+        L.pmhd_perf_roofline_cap.argtypes = [_P(PlatformC), _P(C.c_char_p), _dp, C.c_int, _dp, _ip]
+        L.pmhd_perf_arch_efficiency.argtypes = [C.c_double, C.c_double, _dp, _ip]
+        L.pmhd_perf_pp_metric.argtypes = [_dp, _ip, C.c_int, _dp]
         _host = L
     return _host
 

@@ -30,11 +30,21 @@ for n in [int(a) for a in sys.argv[1:]] or [64, 128, 256]:
     f = O.flops()
     reg = O.region_flops()
     cells = cfg.active_cells
+    regions = {name: float(v) / cells for name, v in zip(O.REGIONS, reg)}
+    regions["dt"] = (float(f.sum()) - float(reg.sum())) / cells
     res[str(n)] = {"add": f[0], "mul": f[1], "div": f[2], "sqrt": f[3], "total": float(f.sum()),
                    "per_cell_update": float(f.sum()) / cells,
-                   "flux_region_per_cell_update": reg[0] / cells,
-                   "update_region_per_cell_update": (float(f.sum()) - reg[0]) / cells,
+                   "flux_region_per_cell_update": float(reg[:3].sum()) / cells,
+                   "update_region_per_cell_update": (float(f.sum()) - float(reg[:3].sum())) / cells,
+                   "regions_per_cell_update": regions,
                    "seconds": time.time() - t0}
     print(n, res[str(n)], flush=True)
     del s
 json.dump(res, open(out_path, "w"), indent=1)
+# region table for the CLI's roofline / report commands (per cell-update, largest size)
+big = res[str(max(int(k) for k in res))]
+if "regions_per_cell_update" in big:
+    with open(os.path.join(ROOT, "profiles", "falg_regions.csv"), "w") as fh:
+        fh.write("region,flops_per_cell_update\n")
+        for name, v in big["regions_per_cell_update"].items():
+            fh.write(f"{name},{v!r}\n")
