@@ -192,6 +192,25 @@ int pmhd_gpu_halo_unpack(pmhd_mesh* mesh, int gid, int dir, int side, int half, 
  * (default): every call returns once its results are complete. */
 int pmhd_gpu_set_async(pmhd_mesh* mesh, int on);
 
+/* Turbulence driving (definition in pmhd_host.h).  One
+ * event = three calls; the caller combines the per-block partial sums over
+ * all blocks in gid order (across ranks too), so every decomposition and the
+ * CPU oracle form the same bits:
+ *  1 drive_begin: nmode modes (k: nmode x 3 ints, c / s: nmode x 3 doubles)
+ *    and the per-axis phase tables (host pointers, 5 x nx[a] doubles each);
+ *    forms dv on every active cell and returns sums[4 b + q] =
+ *    (sum rho, sum rho dv_x, sum rho dv_y, sum rho dv_z) of local block b,
+ *    each (k, j) row summed over i, rows in (k, j) order;
+ *  2 drive_energy(mean): dv' = dv - mean; sums[4 b + q] =
+ *    (sum 1/2 rho |dv'|^2, sum m.dv', 0, 0);
+ *  3 drive_apply(mean, s): m += (s rho) dv', E += KE(m_new) - KE(m), then the
+ *    ghost exchange of blocks with local neighbours (multi-rank callers
+ *    exchange the rest). */
+int pmhd_gpu_drive_begin(pmhd_mesh* mesh, int nmode, const int* k, const double* c, const double* s,
+                         const double* const* cos_tab, const double* const* sin_tab, double* sums);
+int pmhd_gpu_drive_energy(pmhd_mesh* mesh, const double* mean, double* sums);
+int pmhd_gpu_drive_apply(pmhd_mesh* mesh, const double* mean, double scale);
+
 /* Diagnostics (PMHD_DIAG_*). */
 int pmhd_gpu_diag(pmhd_mesh* mesh, int kind, double* out);
 

@@ -57,6 +57,12 @@ typedef struct pmhd_run_config {
   double tlim;              /* time limit (<= 0: one wave period / pgen default) */
   int workers;              /* CPU workers (oracle / baseline)                  */
   int gpus;
+  /* turbulence driving (BASELINE config 5 "driven"):
+   * every turb_every cycles, a solenoidal velocity impulse injecting
+   * turb_dedt x (time since the last event) of kinetic energy */
+  int turb_drive;           /* 0: decaying (default), 1: driven                 */
+  double turb_dedt;         /* energy injection rate, default 1                 */
+  int turb_every;           /* cycles between driving events, default 1         */
 } pmhd_run_config;
 
 /* Defaults (empty text -> 16^3, one block). */
@@ -108,6 +114,29 @@ int pmhd_host_snapshot_write(const char* path, const pmhd_run_config* cfg, doubl
                              double* const* b3f);
 int pmhd_host_snapshot_read(const char* path, const pmhd_run_config* cfg, double* t, double* const* u,
                             double* const* b1f, double* const* b2f, double* const* b3f);
+
+/* ---- Turbulence driving ---------------------------------
+ * Impulsive solenoidal forcing: event e draws Fourier modes with integer
+ * wavevectors 1 <= |k|^2 <= 4 (half space) from mt19937_64(turb_seed ^
+ * (e+1) * golden) in the fixed (kx,ky,kz) loop order of the turbulence pgen;
+ * dv(x) = sum_m c_m cos(2 pi k.x/L) + s_m sin(2 pi k.x/L), c_m and s_m
+ * projected perpendicular to k.  cos/sin are products of per-axis tables
+ * (k = -2..2 at the global cell centres), so every backend forms the same
+ * bits. */
+#define PMHD_DRIVE_MAX_MODES 64
+typedef struct pmhd_drive_modes {
+  int n;
+  int k[PMHD_DRIVE_MAX_MODES][3];
+  double c[PMHD_DRIVE_MAX_MODES][3];
+  double s[PMHD_DRIVE_MAX_MODES][3];
+} pmhd_drive_modes;
+int pmhd_host_drive_modes(const pmhd_run_config* cfg, long long event, pmhd_drive_modes* out);
+/* axis table: cos_tab[(k+2)*nx + g], sin_tab[...] for k = -2..2 and the
+ * global cell index g in [0, nx[axis]) */
+int pmhd_host_drive_tables(const pmhd_run_config* cfg, int axis, double* cos_tab, double* sin_tab);
+/* impulse amplitude s >= 0 with a s^2 + b s = de (a = sum 1/2 rho |dv'|^2,
+ * b = sum rho v.dv'): s = (-b + sqrt(b^2 + 4 a de)) / (2 a) */
+double pmhd_host_drive_scale(double a, double b, double de);
 
 /* ---- perf_model: roofline (Eq. 1), architectural
  * efficiency (Eq. 2), performance-portability metric (Eq. 3) over platform

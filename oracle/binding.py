@@ -36,6 +36,10 @@ def lib(ref: bool = False) -> C.CDLL:
         L.oracle_halo_count.restype = C.c_longlong
         L.oracle_halo_pack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         L.oracle_halo_unpack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        _ip = C.POINTER(C.c_int)
+        L.oracle_drive_begin.argtypes = [C.c_void_p, C.c_int, _ip, _dp, _dp, C.POINTER(_dp), C.POINTER(_dp), _dp]
+        L.oracle_drive_energy.argtypes = [C.c_void_p, _dp, _dp]
+        L.oracle_drive_apply.argtypes = [C.c_void_p, _dp, C.c_double]
         L.oracle_mesh_destroy.argtypes = [C.c_void_p]
         L.oracle_mesh_destroy.restype = None
         L.oracle_set_workers.argtypes = [C.c_int]
@@ -179,6 +183,25 @@ class OracleSolver:
 
     def halo_unpack(self, gid, d, side, half, buf):
         self.L.oracle_halo_unpack(self.h, gid, d, side, int(half), C.cast(buf.data_ptr(), _dp))
+
+    # ---- turbulence driving (pmhd_gpu.h drive_* semantics) -------------------
+    def drive_begin(self, k, c, s, ct, st):
+        sums = np.zeros((len(self.gids), 4))
+        cp = (_dp * 3)(*[t.ctypes.data_as(_dp) for t in ct])
+        sp = (_dp * 3)(*[t.ctypes.data_as(_dp) for t in st])
+        self.L.oracle_drive_begin(self.h, len(k), k.ctypes.data_as(C.POINTER(C.c_int)), c.ctypes.data_as(_dp),
+                                  s.ctypes.data_as(_dp), cp, sp, sums.ctypes.data_as(_dp))
+        return sums
+
+    def drive_energy(self, mean):
+        sums = np.zeros((len(self.gids), 4))
+        m = np.asarray(mean, dtype=np.float64)
+        self.L.oracle_drive_energy(self.h, m.ctypes.data_as(_dp), sums.ctypes.data_as(_dp))
+        return sums
+
+    def drive_apply(self, mean, scale):
+        m = np.asarray(mean, dtype=np.float64)
+        self.L.oracle_drive_apply(self.h, m.ctypes.data_as(_dp), float(scale))
 
     def close(self):
         if self.h:

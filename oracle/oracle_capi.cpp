@@ -42,6 +42,10 @@ struct MeshBase {
   virtual size_t pack(int gid, int dir, int side, bool half, double* out) = 0;
   virtual size_t unpack(int gid, int dir, int side, bool half, const double* in) = 0;
   virtual int local_of(int gid) const = 0;
+  virtual void drive_begin(int n, const int* k, const double* c, const double* s, const double* const* ct,
+                           const double* const* st, double* sums) = 0;
+  virtual void drive_energy(const double* mean, double* sums) = 0;
+  virtual void drive_apply(const double* mean, double scale) = 0;
 };
 
 template <class R>
@@ -52,6 +56,12 @@ struct MeshImpl final : MeshBase {
     m.stage(s, dt, bad, nf, false);
   }
   void sweep(int dir, bool half) override { m.sweep(dir, half); }
+  void drive_begin(int n, const int* k, const double* c, const double* s, const double* const* ct,
+                   const double* const* st, double* sums) override {
+    m.drive_begin(n, k, c, s, ct, st, sums);
+  }
+  void drive_energy(const double* mean, double* sums) override { m.drive_energy(mean, sums); }
+  void drive_apply(const double* mean, double scale) override { m.drive_apply(mean, scale); }
   size_t halo_count(int dir, int side) const override { return m.halo_count(dir, side); }
   size_t pack(int gid, int dir, int side, bool half, double* out) override {
     return m.pack(gid, dir, side, half, out);
@@ -304,6 +314,21 @@ int oracle_face_data(oracle_mesh* m, int gid, int dir, double* out) {
 }
 int oracle_emf_data(oracle_mesh* m, int gid, int comp, double* out) {
   m->impl->emf_data(gid, comp, out);
+  return PMHD_OK;
+}
+
+// Turbulence driving (pmhd_gpu.h drive_* semantics, CPU restatement).
+int oracle_drive_begin(oracle_mesh* m, int n, const int* k, const double* c, const double* s,
+                       const double* const* ct, const double* const* st, double* sums) {
+  m->impl->drive_begin(n, k, c, s, ct, st, sums);
+  return PMHD_OK;
+}
+int oracle_drive_energy(oracle_mesh* m, const double* mean, double* sums) {
+  m->impl->drive_energy(mean, sums);
+  return PMHD_OK;
+}
+int oracle_drive_apply(oracle_mesh* m, const double* mean, double scale) {
+  m->impl->drive_apply(mean, scale);
   return PMHD_OK;
 }
 

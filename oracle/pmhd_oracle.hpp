@@ -904,6 +904,99 @@ class Mesh {
     for (int dir = 0; dir < g.dim; ++dir) sweep(dir, use_B);
   }
 
+  //--------------------------------------------------------------------------
+  // Turbulence driving (definition in include/pmhd_host.h,
+  // GPU: kernels_drive.cu).  dv per local block on active cells; sums per
+  // block with each (k, j) row summed over i and rows in (k, j) order.
+  std::vector<Field<R>> dvel;  // 3 per local block
+
+  void drive_begin(int nmode, const int* kv, const double* cv, const double* sv,
+                   const double* const* ct, const double* const* st, double* sums) {
+    dvel.assign(3 * blocks.size(), Field<R>());
+    for (size_t b = 0; b < blocks.size(); ++b) {
+      Block<R>& B = blocks[b];
+      Field<R>* D = &dvel[3 * b];
+      for (int a = 0; a < 3; ++a) D[a].resize(g.n[2], g.n[1], g.n[0]);
+      R s0 = R(0.0), s1 = R(0.0), s2 = R(0.0), s3 = R(0.0);
+      for (int k = g.ks; k < g.ke; ++k)
+        for (int j = g.js; j < g.je; ++j) {
+          R r0 = R(0.0), r1 = R(0.0), r2 = R(0.0), r3 = R(0.0);
+          for (int i = g.is; i < g.ie; ++i) {
+            const int gi = B.c[0] * g.mb[0] + (i - g.is), gj = B.c[1] * g.mb[1] + (j - g.js);
+            const int gk = (g.dim == 3) ? B.c[2] * g.mb[2] + (k - g.ks) : 0;
+            R dv0 = R(0.0), dv1 = R(0.0), dv2 = R(0.0);
+            for (int m = 0; m < nmode; ++m) {
+              const int qx = (kv[3 * m] + 2) * g.nx[0] + gi;
+              const int qy = (kv[3 * m + 1] + 2) * g.nx[1] + gj;
+              const int qz = (kv[3 * m + 2] + 2) * g.nx[2] + gk;
+              const R axr = ct[0][qx], axi = st[0][qx], ayr = ct[1][qy], ayi = st[1][qy];
+              const R azr = ct[2][qz], azi = st[2][qz];
+              const R zr = axr * ayr - axi * ayi, zi = axr * ayi + axi * ayr;
+              const R cr = zr * azr - zi * azi, ci = zr * azi + zi * azr;
+              dv0 = dv0 + (cv[3 * m] * cr + sv[3 * m] * ci);
+              dv1 = dv1 + (cv[3 * m + 1] * cr + sv[3 * m + 1] * ci);
+              dv2 = dv2 + (cv[3 * m + 2] * cr + sv[3 * m + 2] * ci);
+            }
+            D[0](k, j, i) = dv0;
+            D[1](k, j, i) = dv1;
+            D[2](k, j, i) = dv2;
+            const R rho = B.A.u[IDN](k, j, i);
+            r0 = r0 + rho;
+            r1 = r1 + rho * dv0;
+            r2 = r2 + rho * dv1;
+            r3 = r3 + rho * dv2;
+          }
+          s0 = s0 + r0; s1 = s1 + r1; s2 = s2 + r2; s3 = s3 + r3;
+        }
+      sums[4 * b] = value_of(s0); sums[4 * b + 1] = value_of(s1); sums[4 * b + 2] = value_of(s2); sums[4 * b + 3] = value_of(s3);
+    }
+  }
+
+  void drive_energy(const double* mean, double* sums) {
+    for (size_t b = 0; b < blocks.size(); ++b) {
+      Block<R>& B = blocks[b];
+      const Field<R>* D = &dvel[3 * b];
+      R s0 = R(0.0), s1 = R(0.0);
+      for (int k = g.ks; k < g.ke; ++k)
+        for (int j = g.js; j < g.je; ++j) {
+          R r0 = R(0.0), r1 = R(0.0);
+          for (int i = g.is; i < g.ie; ++i) {
+            const R rho = B.A.u[IDN](k, j, i);
+            const R p0 = D[0](k, j, i) - mean[0], p1 = D[1](k, j, i) - mean[1], p2 = D[2](k, j, i) - mean[2];
+            const R q = p0 * p0 + p1 * p1 + p2 * p2;
+            r0 = r0 + 0.5 * rho * q;
+            r1 = r1 + (B.A.u[IM1](k, j, i) * p0 + B.A.u[IM2](k, j, i) * p1 + B.A.u[IM3](k, j, i) * p2);
+          }
+          s0 = s0 + r0; s1 = s1 + r1;
+        }
+      sums[4 * b] = value_of(s0); sums[4 * b + 1] = value_of(s1); sums[4 * b + 2] = 0.0; sums[4 * b + 3] = 0.0;
+    }
+  }
+
+  void drive_apply(const double* mean, double scale) {
+    for (size_t b = 0; b < blocks.size(); ++b) {
+      Block<R>& B = blocks[b];
+      const Field<R>* D = &dvel[3 * b];
+      for (int k = g.ks; k < g.ke; ++k)
+        for (int j = g.js; j < g.je; ++j)
+          for (int i = g.is; i < g.ie; ++i) {
+            const R rho = B.A.u[IDN](k, j, i);
+            const R p0 = D[0](k, j, i) - mean[0], p1 = D[1](k, j, i) - mean[1], p2 = D[2](k, j, i) - mean[2];
+            const R a0 = B.A.u[IM1](k, j, i), a1 = B.A.u[IM2](k, j, i), a2 = B.A.u[IM3](k, j, i);
+            const R sr = scale * rho;
+            const R n0 = a0 + sr * p0, n1 = a1 + sr * p1, n2 = a2 + sr * p2;
+            const R irho = 1.0 / rho;
+            const R ke0 = 0.5 * (a0 * a0 + a1 * a1 + a2 * a2) * irho;
+            const R ke1 = 0.5 * (n0 * n0 + n1 * n1 + n2 * n2) * irho;
+            B.A.u[IM1](k, j, i) = n0;
+            B.A.u[IM2](k, j, i) = n1;
+            B.A.u[IM3](k, j, i) = n2;
+            B.A.u[IEN](k, j, i) = B.A.u[IEN](k, j, i) + (ke1 - ke0);
+          }
+    }
+    exchange(false);
+  }
+
   // Ghost range that block side r receives in direction dir, for array v
   // (0..4 cells, 5..7 faces b1f..b3f): [q0, q1) along dir.  The sender's
   // range is the same shifted by +m (r = 0, from the lower neighbour) or -m.

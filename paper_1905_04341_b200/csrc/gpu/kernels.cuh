@@ -72,6 +72,20 @@ struct HaloSlab {
 };
 void launch_halo_copy(double* const* dev_arrays, const KGeom& G, const HaloSlab& sl, double* buf,
                       int to_buf, cudaStream_t s);
+// Turbulence driving (kernels_drive.cu): device copies of the modes and the
+// per-axis phase tables (pmhd_host.h pmhd_drive_modes / drive_tables).
+struct DriveTabs {
+  int n;
+  int k[64][3];
+  double c[64][3], s[64][3];
+  const double* ct[3];  // cos tables, (k+2)*nx[a] + g
+  const double* st[3];  // sin tables
+};
+void launch_drive_dv(const DevBlock* blks, const KGeom& G, const DriveTabs& T, cudaStream_t s);
+void launch_drive_sums(const DevBlock* blks, const KGeom& G, int mode, const double mean[3], double* rows,
+                       double* sums, cudaStream_t s);
+void launch_drive_apply(const DevBlock* blks, const KGeom& G, const double mean[3], double scale,
+                        cudaStream_t s);
 void launch_repack(double* dense, double* pitched, const KGeom& G, int e1, int e2, int e3,
                    int to_dense, cudaStream_t s);
 void launch_bcc_dense(double* dense, const double* bf, const KGeom& G, int c, cudaStream_t s);

@@ -54,6 +54,11 @@ struct pmhd_mesh {
   bool all_local = true;
   bool prof = false;
   bool async_ops = false;         // pmhd_gpu_set_async: stream-ordered multi-rank calls
+  // turbulence driving buffers (allocated at the first event)
+  double* drive_tab = nullptr;    // 3 axes x (cos, sin) x 5 x nx[a]
+  double* drive_rows = nullptr;   // nb x rows x 4
+  double* drive_sums = nullptr;   // nb x 4
+  DriveTabs drive{};
   int variant = 0;                // 0: fused flux kernels; 1: split (debug; PMHD_KERNELS=split)
   int slab_planes = 0;            // k-slab pipeline depth (PMHD_SLAB_PLANES, 0 = off)
   std::vector<cudaEvent_t> slab_ev;
@@ -457,6 +462,7 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   cudaSetDevice(m->ctx->device);
   cudaStreamSynchronize(m->ctx->stream);
   cudaFree(m->slab);
+  if (m->drive_tab) { cudaFree(m->drive_tab); cudaFree(m->drive_rows); cudaFree(m->drive_sums); }
   cudaFree(m->dblk);
   cudaFree(m->dblk_alt);
   cudaFree(m->dred);
@@ -711,6 +717,71 @@ int pmhd_gpu_stage_compute(pmhd_mesh* m, int stage, double dt, double* dt_next, 
   if (!rc) rc = enqueue_stage(m, stage, dt, false);
   if (rc) return rc;
   return finish(m, stage, stage, stage == 2 ? dt_next : nullptr, st);
+}
+
+int pmhd_gpu_drive_begin(pmhd_mesh* m, int nmode, const int* k, const double* c, const double* s,
+                         const double* const* cos_tab, const double* const* sin_tab, double* sums) {
+  if (!m || nmode < 0 || nmode > 64 || (nmode > 0 && (!k || !c || !s)) || !cos_tab || !sin_tab || !sums)
+    return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  const KGeom& G = m->G;
+  if (!m->drive_tab) {
+    const size_t tab = 2 * 5 * size_t(G.nx[0] + G.nx[1] + G.nx[2]);
+    const size_t rows = size_t(G.nb) * (G.ke - G.ks) * (G.je - G.js) * 4;
+    CK(cudaMalloc(&m->drive_tab, tab * sizeof(double)));
+    CK(cudaMalloc(&m->drive_rows, rows * sizeof(double)));
+    CK(cudaMalloc(&m->drive_sums, size_t(G.nb) * 4 * sizeof(double)));
+  }
+  DriveTabs& T = m->drive;
+  T.n = nmode;
+  for (int q = 0; q < nmode; ++q)
+    for (int a = 0; a < 3; ++a) {
+      T.k[q][a] = k[3 * q + a];
+      T.c[q][a] = c[3 * q + a];
+      T.s[q][a] = s[3 * q + a];
+    }
+  double* p = m->drive_tab;
+  for (int a = 0; a < 3; ++a) {
+    const size_t n = 5 * size_t(G.nx[a]);
+    CK(cudaMemcpyAsync(p, cos_tab[a], n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    T.ct[a] = p;
+    p += n;
+    CK(cudaMemcpyAsync(p, sin_tab[a], n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    T.st[a] = p;
+    p += n;
+  }
+  launch_drive_dv(m->dblk, G, T, ctx->stream);
+  const double zero[3] = {0.0, 0.0, 0.0};
+  launch_drive_sums(m->dblk, G, 0, zero, m->drive_rows, m->drive_sums, ctx->stream);
+  m->times.kernel_launches += 3;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(sums, m->drive_sums, size_t(G.nb) * 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PMHD_OK;
+}
+
+int pmhd_gpu_drive_energy(pmhd_mesh* m, const double* mean, double* sums) {
+  if (!m || !mean || !sums || !m->drive_tab) return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  launch_drive_sums(m->dblk, m->G, 1, mean, m->drive_rows, m->drive_sums, ctx->stream);
+  m->times.kernel_launches += 2;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(sums, m->drive_sums, size_t(m->G.nb) * 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PMHD_OK;
+}
+
+int pmhd_gpu_drive_apply(pmhd_mesh* m, const double* mean, double scale) {
+  if (!m || !mean || !m->drive_tab) return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  launch_drive_apply(m->dblk, m->G, mean, scale, ctx->stream);
+  launch_exchange(m->dblk, m->G, 0, ctx->stream);
+  m->times.kernel_launches += 1 + m->G.dim;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PMHD_OK;
 }
 
 int pmhd_gpu_set_async(pmhd_mesh* m, int on) {

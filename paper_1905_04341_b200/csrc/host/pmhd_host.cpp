@@ -396,6 +396,9 @@ void pmhd_host_config_defaults(pmhd_run_config* c) {
   c->blast_b[0] = 1.0 / std::sqrt(2.0); c->blast_b[1] = 1.0 / std::sqrt(2.0); c->blast_b[2] = 0.0;
   c->turb_mach = 1.0;
   c->turb_seed = 1905043410ULL;
+  c->turb_drive = 0;
+  c->turb_dedt = 1.0;
+  c->turb_every = 1;
   c->uniform_w[0] = 1.0; c->uniform_w[4] = 0.6;
   c->uniform_w[5] = std::sqrt(0.6);
   c->nlim = -1;
@@ -481,6 +484,9 @@ int pmhd_host_config_parse(const char* text, pmhd_run_config* c, int* err_line, 
     else if (key == "blast_b3") D(&c->blast_b[2]);
     else if (key == "turb_mach") D(&c->turb_mach);
     else if (key == "turb_seed") { double s; D(&s); if (ok) c->turb_seed = (uint64_t)s; }
+    else if (key == "turb_drive") I(&c->turb_drive);
+    else if (key == "turb_dedt") D(&c->turb_dedt);
+    else if (key == "turb_every") I(&c->turb_every);
     else if (key == "rho") D(&c->uniform_w[0]);
     else if (key == "v1") D(&c->uniform_w[1]); else if (key == "v2") D(&c->uniform_w[2]);
     else if (key == "v3") D(&c->uniform_w[3]); else if (key == "p") D(&c->uniform_w[4]);
@@ -519,7 +525,60 @@ int pmhd_host_validate(const pmhd_run_config* c, char* err, int errlen) {
   }
   if (!(m.gamma > 1.0)) { set_err(err, errlen, "gamma must be > 1"); return PMHD_ERR_CONFIG; }
   if (!(m.cfl > 0.0 && m.cfl < 1.0)) { set_err(err, errlen, "cfl must be in (0,1)"); return PMHD_ERR_CONFIG; }
+  if (c->turb_drive && (c->turb_every < 1 || !(c->turb_dedt >= 0.0))) {
+    set_err(err, errlen, "turb_every must be >= 1 and turb_dedt >= 0");
+    return PMHD_ERR_CONFIG;
+  }
   return PMHD_OK;
+}
+
+//---------------------------------------------------------- turbulence driving
+int pmhd_host_drive_modes(const pmhd_run_config* cfg, long long event, pmhd_drive_modes* out) {
+  if (!cfg || !out || event < 0) return PMHD_ERR_INPUT;
+  std::mt19937_64 rng(cfg->turb_seed ^ (0x9E3779B97F4A7C15ULL * (uint64_t)(event + 1)));
+  const bool d3 = cfg->mesh.nx[2] > 1;
+  out->n = 0;
+  for (int kx = -2; kx <= 2; ++kx)
+    for (int ky = -2; ky <= 2; ++ky)
+      for (int kz = -2; kz <= 2; ++kz) {
+        if (!d3 && kz != 0) continue;
+        const int k2 = kx * kx + ky * ky + kz * kz;
+        if (k2 < 1 || k2 > 4) continue;
+        const bool half = (kx > 0) || (kx == 0 && ky > 0) || (kx == 0 && ky == 0 && kz > 0);
+        if (!half) continue;
+        const int m = out->n++;
+        const int k[3] = {kx, ky, kz};
+        double c[3], sn[3];
+        for (int a = 0; a < 3; ++a) c[a] = 2.0 * u01(rng) - 1.0;
+        for (int a = 0; a < 3; ++a) sn[a] = 2.0 * u01(rng) - 1.0;
+        const double ck = (c[0] * kx + c[1] * ky + c[2] * kz) / double(k2);
+        const double sk = (sn[0] * kx + sn[1] * ky + sn[2] * kz) / double(k2);
+        for (int a = 0; a < 3; ++a) {
+          out->k[m][a] = k[a];
+          out->c[m][a] = c[a] - ck * k[a];
+          out->s[m][a] = sn[a] - sk * k[a];
+        }
+      }
+  return PMHD_OK;
+}
+
+int pmhd_host_drive_tables(const pmhd_run_config* cfg, int axis, double* cos_tab, double* sin_tab) {
+  if (!cfg || axis < 0 || axis > 2 || !cos_tab || !sin_tab) return PMHD_ERR_INPUT;
+  const int n = cfg->mesh.nx[axis];
+  for (int k = -2; k <= 2; ++k)
+    for (int g = 0; g < n; ++g) {
+      // phase of wavenumber k at the centre of global cell g (domain-relative,
+      // so the tables do not depend on the extent)
+      const double th = 2.0 * kPi * double(k) * (double(g) + 0.5) / double(n);
+      cos_tab[(k + 2) * n + g] = std::cos(th);
+      sin_tab[(k + 2) * n + g] = std::sin(th);
+    }
+  return PMHD_OK;
+}
+
+double pmhd_host_drive_scale(double a, double b, double de) {
+  if (!(a > 0.0) || !(de > 0.0)) return 0.0;
+  return (-b + std::sqrt(b * b + 4.0 * a * de)) / (2.0 * a);
 }
 
 int pmhd_host_nblocks(const pmhd_run_config* c) {

@@ -104,6 +104,18 @@ class RunConfigC(C.Structure):
         ("tlim", C.c_double),
         ("workers", C.c_int),
         ("gpus", C.c_int),
+        ("turb_drive", C.c_int),
+        ("turb_dedt", C.c_double),
+        ("turb_every", C.c_int),
+    ]
+
+
+class DriveModesC(C.Structure):
+    _fields_ = [
+        ("n", C.c_int),
+        ("k", (C.c_int * 3) * 64),
+        ("c", (C.c_double * 3) * 64),
+        ("s", (C.c_double * 3) * 64),
     ]
 
 
@@ -152,6 +164,10 @@ def host_lib() -> C.CDLL:
         _pp = _P(_dp)
         L.pmhd_host_snapshot_write.argtypes = [C.c_char_p, _P(RunConfigC), C.c_double, _pp, _pp, _pp, _pp]
         L.pmhd_host_snapshot_read.argtypes = [C.c_char_p, _P(RunConfigC), _dp, _pp, _pp, _pp, _pp]
+        L.pmhd_host_drive_modes.argtypes = [_P(RunConfigC), C.c_longlong, _P(DriveModesC)]
+        L.pmhd_host_drive_tables.argtypes = [_P(RunConfigC), C.c_int, _dp, _dp]
+        L.pmhd_host_drive_scale.argtypes = [C.c_double, C.c_double, C.c_double]
+        L.pmhd_host_drive_scale.restype = C.c_double
         L.pmhd_perf_load_platforms.argtypes = [C.c_char_p, _P(PlatformC), C.c_int, _ip, _ip, C.c_char_p,
                                                C.c_int]
         L.pmhd_perf_format_platforms.argtypes = [_P(PlatformC), C.c_int, C.c_char_p, C.c_int]
@@ -170,6 +186,7 @@ GPU_SYMBOLS = [
     "pmhd_gpu_run", "pmhd_gpu_diag", "pmhd_gpu_set_profiling", "pmhd_gpu_region_times",
     "pmhd_gpu_build_info", "pmhd_gpu_stream", "pmhd_gpu_stage_compute", "pmhd_gpu_exchange_dir",
     "pmhd_gpu_halo_count", "pmhd_gpu_halo_pack", "pmhd_gpu_halo_unpack", "pmhd_gpu_set_async",
+    "pmhd_gpu_drive_begin", "pmhd_gpu_drive_energy", "pmhd_gpu_drive_apply",
 ]
 
 
@@ -215,6 +232,9 @@ def gpu_lib(parity: bool = False) -> C.CDLL:
         L.pmhd_gpu_halo_pack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.pmhd_gpu_halo_unpack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.pmhd_gpu_set_async.argtypes = [C.c_void_p, C.c_int]
+        L.pmhd_gpu_drive_begin.argtypes = [C.c_void_p, C.c_int, _ip, _dp, _dp, _P(_dp), _P(_dp), _dp]
+        L.pmhd_gpu_drive_energy.argtypes = [C.c_void_p, _dp, _dp]
+        L.pmhd_gpu_drive_apply.argtypes = [C.c_void_p, _dp, C.c_double]
         L.pmhd_gpu_stream.argtypes = [C.c_void_p]
         L.pmhd_gpu_stream.restype = C.c_void_p
         L.pmhd_gpu_build_info.argtypes = []

@@ -163,6 +163,28 @@ class GpuSolver:
     def halo_pack(self, gid, d, side, half, buf):
         self._check(self.L.pmhd_gpu_halo_pack(self.mesh, gid, d, side, int(half), C.c_void_p(buf.data_ptr())))
 
+    # ---- turbulence driving (pmhd_gpu.h drive_*; orchestration in drive.py) ----
+    def drive_begin(self, k, c, s, ct, st):
+        import numpy as np
+        sums = np.zeros((len(self.gids), 4))
+        cp = (N._dp * 3)(*[N.dptr(t) for t in ct])
+        sp = (N._dp * 3)(*[N.dptr(t) for t in st])
+        self._check(self.L.pmhd_gpu_drive_begin(self.mesh, len(k), k.ctypes.data_as(N._ip), N.dptr(c),
+                                                N.dptr(s), cp, sp, N.dptr(sums)))
+        return sums
+
+    def drive_energy(self, mean):
+        import numpy as np
+        sums = np.zeros((len(self.gids), 4))
+        self._check(self.L.pmhd_gpu_drive_energy(self.mesh, N.dptr(np.asarray(mean, dtype=np.float64)),
+                                                 N.dptr(sums)))
+        return sums
+
+    def drive_apply(self, mean, scale):
+        import numpy as np
+        self._check(self.L.pmhd_gpu_drive_apply(self.mesh, N.dptr(np.asarray(mean, dtype=np.float64)),
+                                                float(scale)))
+
     def set_async(self, on=True):
         """Stream-ordered multi-rank mode (pmhd_gpu_set_async)."""
         self._check(self.L.pmhd_gpu_set_async(self.mesh, int(on)))
