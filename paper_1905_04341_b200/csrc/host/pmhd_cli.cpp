@@ -18,6 +18,7 @@
 // errors exit non-zero.
 #include <sys/stat.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -70,6 +71,76 @@ struct Blocks {
     b3.assign(nb, std::vector<double>(n3f));
   }
 };
+
+// Turbulence driving: the host side of one forcing event
+// over the drive_* ABI; sums combined over blocks in gid order.
+struct Drive {
+  const pmhd_run_config* cfg = nullptr;
+  std::vector<double> ct[3], st[3];
+  long long event = 0;
+  double since = 0.0;  // time since the last event
+  void init(const pmhd_run_config& c) {
+    cfg = &c;
+    for (int a = 0; a < 3; ++a) {
+      ct[a].assign(5 * size_t(c.mesh.nx[a]), 0.0);
+      st[a].assign(5 * size_t(c.mesh.nx[a]), 0.0);
+      pmhd_host_drive_tables(&c, a, ct[a].data(), st[a].data());
+    }
+  }
+  int kick(pmhd_mesh* mesh, int nb) {
+    pmhd_drive_modes md;
+    pmhd_host_drive_modes(cfg, event, &md);
+    std::vector<int> k(3 * md.n);
+    std::vector<double> c(3 * md.n), s(3 * md.n), sums(4 * size_t(nb));
+    for (int m = 0; m < md.n; ++m)
+      for (int a = 0; a < 3; ++a) {
+        k[3 * m + a] = md.k[m][a];
+        c[3 * m + a] = md.c[m][a];
+        s[3 * m + a] = md.s[m][a];
+      }
+    const double* cp[3] = {ct[0].data(), ct[1].data(), ct[2].data()};
+    const double* sp[3] = {st[0].data(), st[1].data(), st[2].data()};
+    int rc = pmhd_gpu_drive_begin(mesh, md.n, k.data(), c.data(), s.data(), cp, sp, sums.data());
+    if (rc) return rc;
+    double tot[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int b = 0; b < nb; ++b)
+      for (int q = 0; q < 4; ++q) tot[q] = tot[q] + sums[4 * b + q];
+    const double mean[3] = {tot[1] / tot[0], tot[2] / tot[0], tot[3] / tot[0]};
+    rc = pmhd_gpu_drive_energy(mesh, mean, sums.data());
+    if (rc) return rc;
+    double te[2] = {0.0, 0.0};
+    for (int b = 0; b < nb; ++b)
+      for (int q = 0; q < 2; ++q) te[q] = te[q] + sums[4 * b + q];
+    const double cells = double(cfg->mesh.nx[0]) * cfg->mesh.nx[1] * cfg->mesh.nx[2];
+    const double scale = pmhd_host_drive_scale(te[0], te[1], cfg->turb_dedt * since * cells);
+    rc = pmhd_gpu_drive_apply(mesh, mean, scale);
+    ++event;
+    since = 0.0;
+    return rc;
+  }
+};
+
+// cmd_run / cmd_bench cycle loop; with turb_drive, chunks of turb_every
+// cycles separated by forcing events (dt recomputed after each).
+int run_cycles(pmhd_mesh* mesh, const pmhd_run_config& cfg, Drive* drv, int nb, int ncycles, double tlim,
+               double* t, double* dt, int* done, pmhd_status* st) {
+  if (!cfg.turb_drive) return pmhd_gpu_run(mesh, ncycles, tlim, t, dt, done, st);
+  *done = 0;
+  while ((ncycles < 0 || *done < ncycles) && (tlim <= 0.0 || *t < tlim)) {
+    int chunk = cfg.turb_every;
+    if (ncycles >= 0) chunk = std::min(chunk, ncycles - *done);
+    const double t0 = *t;
+    int d = 0;
+    const int rc = pmhd_gpu_run(mesh, chunk, tlim, t, dt, &d, st);
+    if (rc) return rc;
+    *done += d;
+    drv->since += *t - t0;
+    if (d < chunk || d == 0) break;  // reached tlim
+    if (drv->kick(mesh, nb)) return PMHD_ERR_CUDA;
+    *dt = 0.0;  // recompute after the kick
+  }
+  return PMHD_OK;
+}
 
 // Algorithmic flops per cell-update by region (tools/count_falg.py: the CPU
 // oracle on the CountingScalar restatement, one cycle of the bench config).
@@ -277,12 +348,14 @@ int main(int argc, char** argv) {
   const long long cells = (long long)cfg.mesh.nx[0] * cfg.mesh.nx[1] * cfg.mesh.nx[2];
   pmhd_status st;
   int done = 0;
+  Drive drv;
+  if (cfg.turb_drive) drv.init(cfg);
 
   if (a.cmd == "bench") {
     // cmd_bench: warm-up cycles, then timed cycles; CSV row
-    int rc = pmhd_gpu_run(mesh, a.warmup, -1.0, &t, &dt, &done, &st);
+    int rc = run_cycles(mesh, cfg, &drv, nb, a.warmup, -1.0, &t, &dt, &done, &st);
     auto t0 = std::chrono::steady_clock::now();
-    if (!rc) rc = pmhd_gpu_run(mesh, a.cycles, -1.0, &t, &dt, &done, &st);
+    if (!rc) rc = run_cycles(mesh, cfg, &drv, nb, a.cycles, -1.0, &t, &dt, &done, &st);
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (rc) {
       std::fprintf(stderr, "solver error %d: %s\n", rc, pmhd_gpu_last_error(ctx));
@@ -299,7 +372,7 @@ int main(int argc, char** argv) {
   // cmd_run
   const double tlim = pmhd_host_default_tlim(&cfg);
   auto t0 = std::chrono::steady_clock::now();
-  int rc = pmhd_gpu_run(mesh, cfg.nlim, tlim, &t, &dt, &done, &st);
+  int rc = run_cycles(mesh, cfg, &drv, nb, cfg.nlim, tlim, &t, &dt, &done, &st);
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (rc == PMHD_ERR_UNPHYSICAL) {
     std::fprintf(stderr, "unphysical state in stage 'stage%d' at cell (k=%d, j=%d, i=%d)\n", st.stage,
