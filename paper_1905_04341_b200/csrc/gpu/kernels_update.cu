@@ -19,10 +19,13 @@ namespace pmhd_gpu {
 
 namespace {
 
-constexpr int UX = 32, UY = 8, UTHR = 256;
+#ifndef PMHD_UPDATE_UY
+#define PMHD_UPDATE_UY 8  // tile rows (one thread per cell: 32 x UY threads)
+#endif
+constexpr int UX = 32, UY = PMHD_UPDATE_UY, UTHR = UX * UY;
 constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0-1 .. j1)
 #ifndef PMHD_UPDATE_MINB
-#define PMHD_UPDATE_MINB 5  // resident CTAs per SM the register budget targets (48 regs)
+#define PMHD_UPDATE_MINB (1280 / (32 * PMHD_UPDATE_UY))  // 40 warps/SM of budget (48 regs)
 #endif
 #ifndef PMHD_UPDATE_SEG
 #define PMHD_UPDATE_SEG 16  // max k planes marched by one CTA (shorter for small meshes)
@@ -33,19 +36,34 @@ constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0
 // recomputed: the cell-centred E ring holds planes k and k+1 (one new plane
 // loaded per step), E1 / E2 at k+1/2 become the k-1/2 values of the next
 // step, and so does the new b3 face at k+1.
+// Shared memory of one CTA (dynamic: > 48 KB for 32 x 16 tiles).
+struct UpdSmem {
+  double ec[3][2][EY][EX];      // cell-centred E: [component][k & 1][j][i]
+  double e3s[UY + 1][UX + 1];   // E3 at (k, j-1/2, i-1/2)
+  double e1s[2][UY + 1][UX];    // E1 at (k -/+ 1/2, j-1/2, i), slot by parity
+  double e2s[2][UY][UX + 1];    // E2 at (k -/+ 1/2, j, i-1/2)
+  double b1s[UY][UX + 1];
+  double b2s[UY + 1][UX];
+  double b3s[2][UY][UX];        // new b3 at faces k / k+1, slot by parity
+  double redbuf[UTHR / 32];
+  long long tph[3];             // profiling (thread 0): mark, EMF cycles, update cycles
+};
+
 template <int SEG, bool PROF>
 __global__ void __launch_bounds__(UTHR, PMHD_UPDATE_MINB)
 k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, DevRed* red,
                int want_dt, int kr0, int kr1) {
-  __shared__ double ec[3][2][EY][EX];      // [component][k & 1][j][i]
-  __shared__ double e3s[UY + 1][UX + 1];   // E3 at (k, j-1/2, i-1/2)
-  __shared__ double e1s[2][UY + 1][UX];    // E1 at (k -/+ 1/2, j-1/2, i), slot by parity
-  __shared__ double e2s[2][UY][UX + 1];    // E2 at (k -/+ 1/2, j, i-1/2)
-  __shared__ double b1s[UY][UX + 1];
-  __shared__ double b2s[UY + 1][UX];
-  __shared__ double b3s[2][UY][UX];        // new b3 at faces k / k+1, slot by parity
-  __shared__ double redbuf[UTHR / 32];
-  __shared__ long long tph[3];  // profiling (thread 0): mark, EMF cycles, update cycles
+  extern __shared__ __align__(16) unsigned char upd_smem[];
+  UpdSmem& SM = *reinterpret_cast<UpdSmem*>(upd_smem);
+  auto& ec = SM.ec;
+  auto& e3s = SM.e3s;
+  auto& e1s = SM.e1s;
+  auto& e2s = SM.e2s;
+  auto& b1s = SM.b1s;
+  auto& b2s = SM.b2s;
+  auto& b3s = SM.b3s;
+  auto& redbuf = SM.redbuf;
+  auto& tph = SM.tph;
   if (PROF && threadIdx.x == 0) { tph[0] = clock64(); tph[1] = tph[2] = 0; }
 
   const bool d3 = (G.dim == 3);
@@ -266,12 +284,19 @@ void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, 
   const int seg = (fit >= PMHD_UPDATE_SEG) ? PMHD_UPDATE_SEG : (fit >= 4 ? 4 : 1);
   const int nseg = (nk + seg - 1) / seg;
   const dim3 grid((G.ie - G.is + UX - 1) / UX, (G.je - G.js + UY - 1) / UY, nseg * G.nb);
-#define PMHD_UPDATE_LAUNCH(SG)                                                                    \
-  do {                                                                                            \
-    if (ph.prof)                                                                                  \
-      k_update_fused<SG, true><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);   \
-    else                                                                                          \
-      k_update_fused<SG, false><<<grid, UTHR, 0, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);  \
+  constexpr int smem = (int)sizeof(UpdSmem);
+#define PMHD_UPDATE_LAUNCH(SG)                                                                      \
+  do {                                                                                              \
+    static bool attr = false;                                                                       \
+    if (!attr) {                                                                                    \
+      cudaFuncSetAttribute(k_update_fused<SG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);  \
+      cudaFuncSetAttribute(k_update_fused<SG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      attr = true;                                                                                  \
+    }                                                                                               \
+    if (ph.prof)                                                                                    \
+      k_update_fused<SG, true><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);  \
+    else                                                                                            \
+      k_update_fused<SG, false><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1); \
   } while (0)
   if (seg == PMHD_UPDATE_SEG) PMHD_UPDATE_LAUNCH(PMHD_UPDATE_SEG);
   else if (seg == 4) PMHD_UPDATE_LAUNCH(4);
