@@ -176,6 +176,13 @@ int pmhd_gpu_run(pmhd_mesh* mesh, int ncycles, double tlim, double* t, double* d
  * layout = pack_boundary: variable-major (u0..u4, b1f, b2f,
  * b3f), each slab in k-j-i order.  pack/unpack return after the copy is done. */
 int pmhd_gpu_stage_compute(pmhd_mesh* mesh, int stage, double dt, double* dt_next, pmhd_status* st);
+/* Optional, between stage_compute(1) and the halo exchange that follows it:
+ * enqueue stage 2's flux work on the tiles that read no ghost data (on a
+ * second stream, after stage 1), so it runs while the halo is exchanged;
+ * stage_compute(2, same dt) then does the remaining tiles.  "Overlapped with
+ * interior updates" (north_star); a no-op where it does not apply
+ * (profiling, split kernels, PMHD_OVERLAP=0).  vl2_step does this itself. */
+int pmhd_gpu_stage_prefetch(pmhd_mesh* mesh, int stage, double dt);
 int pmhd_gpu_exchange_dir(pmhd_mesh* mesh, int dir, int half);
 /* doubles in the message that block side `side` (0 lower, 1 upper) receives */
 int pmhd_gpu_halo_count(const pmhd_mesh* mesh, int dir, int side, long long* n);

@@ -168,6 +168,9 @@ class OracleSolver:
         self._check(self.L.oracle_stage_compute(self.h, s, dt, C.byref(dn), C.byref(st)), st)
         return dn.value, st
 
+    def stage_prefetch(self, s, dt):
+        """(GPU overlap hook; nothing to do on the CPU.)"""
+
     def exchange_dir(self, d, half):
         self.L.oracle_exchange_dir(self.h, d, int(half))
 

@@ -95,9 +95,10 @@ void launch_c2p_all(const DevBlock* blks, const KGeom& G, const KPhys& ph, int s
                     int stage, cudaStream_t s);
 void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel, int plm,
                  double c1024, cudaStream_t s);
+// region: 0 all tiles, 1 tiles clear of the ghost exchange, 2 the others
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
                        int plm, double c1024, int stage, DevRed* red, int slab, int nslab, int S,
-                       cudaStream_t s);
+                       cudaStream_t s, int region = 0);
 void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s);
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                          DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s);

@@ -70,7 +70,7 @@ template <int DIR, int RS, bool PROF>
 __global__ void __launch_bounds__(NTHR, FluxMinB<RS>::value)
 k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024,
              int stage, DevRed* red, int write_ec, int f_i0, int f_i1, int f_s0, int f_s1, int f_t0,
-             int f_t1, int ty0) {
+             int f_t1, int ty0, int region) {
   using TS = TileShape<DIR>;
   __shared__ double sw[7][TS::NCELL];  // primitives; after phase 2: q - dq/2 (low-face value)
   __shared__ double sp[7][TS::NCELL];  // after phase 2: q + dq/2 (high-face value)
@@ -85,6 +85,20 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   const int fs0 = f_s0 + (ty0 + blockIdx.y) * FS;  // first face along the 2nd axis
   const DevBlock& B = blks[b];
   double* const* S = B.st[sel];
+  if (region != 0) {
+    // region 1: only tiles whose stencil (cells and the faces their Bcc
+    // averages read) avoids everything the ghost exchange writes -- ghost
+    // cells and the lower normal face s of each axis; region 2: the rest.
+    // Lets the interior tiles of a stage run while the exchange of the
+    // previous stage is in flight.
+    int c0[3], c1[3];  // inclusive cell box (i, j, k) of the tile's stencil
+    if (DIR == 0) { c0[0] = fi0 - 2; c1[0] = fi0 + FX + 1; c0[1] = fs0; c1[1] = fs0 + FS - 1; c0[2] = c1[2] = t3; }
+    else if (DIR == 1) { c0[0] = fi0; c1[0] = fi0 + FX - 1; c0[1] = fs0 - 2; c1[1] = fs0 + FS + 1; c0[2] = c1[2] = t3; }
+    else { c0[0] = fi0; c1[0] = fi0 + FX - 1; c0[2] = fs0 - 2; c1[2] = fs0 + FS + 1; c0[1] = c1[1] = t3; }
+    bool inner = c0[0] >= G.is + 1 && c1[0] <= G.ie - 1 && c0[1] >= G.js + 1 && c1[1] <= G.je - 1;
+    if (G.dim == 3) inner = inner && c0[2] >= G.ks + 1 && c1[2] <= G.ke - 1;
+    if (inner != (region == 1)) return;
+  }
 
   // ---- phase 1: load + cons_to_prim of the stencil cells into smem --------
   // All PER cells' loads are issued before any is consumed (memory-level
@@ -254,7 +268,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 // multiple of the x3 tile's FS (16).  nslab = 1 is the whole block.
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
                        int plm, double c1024, int stage, DevRed* red, int slab, int nslab, int S,
-                       cudaStream_t s) {
+                       cudaStream_t s, int region) {
   const int d3 = (G.dim == 3) ? 1 : 0;
   // face ranges of the oracle: [lo, hi) per axis
   int i0, i1, j0, j1, k0, k1;
@@ -284,10 +298,10 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   do {                                                                                              \
     if (ph.prof)                                                                                    \
       k_flux_fused<D, R, true><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red,      \
-                                                     write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0);    \
+                                                     write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
     else                                                                                            \
       k_flux_fused<D, R, false><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red,     \
-                                                      write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0);   \
+                                                      write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
   } while (0)
 #define PMHD_FLUX_DIRS(R)                          \
   do {                                             \

@@ -54,6 +54,13 @@ struct pmhd_mesh {
   bool all_local = true;
   bool prof = false;
   bool async_ops = false;         // pmhd_gpu_set_async: stream-ordered multi-rank calls
+  // interior-tile prefetch (overlap of a stage's flux work with the previous
+  // stage's ghost exchange): stage whose interior flux tiles are enqueued on
+  // stream2, with the dt they used; ev_pre[0] = input ready, [1] = done
+  int prefetched = 0;
+  double prefetch_dt = 0.0;
+  cudaEvent_t ev_pre[2] = {};
+  bool overlap = false;           // on for meshes with remote neighbours; PMHD_OVERLAP=0/1 overrides
   // turbulence driving buffers (allocated at the first event)
   double* drive_tab = nullptr;    // 3 axes x (cos, sin) x 5 x nx[a]
   double* drive_rows = nullptr;   // nb x rows x 4
@@ -140,10 +147,7 @@ void rec(pmhd_mesh* m, int slot) {
   if (m->prof) cudaEventRecord(m->ev[slot], m->ctx->stream);
 }
 
-// Enqueue one VL2 stage (no synchronization unless profiling).
-int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true) {
-  pmhd_ctx* ctx = m->ctx;
-  const KGeom& G = m->G;
+KStage make_stage(const KGeom& G, int s, double dt) {
   const double beta = (s == 1) ? 0.5 : 1.0;
   const double bdt = beta * dt;
   KStage ks;
@@ -155,7 +159,46 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true) {
   ks.out_sel = (s == 1) ? 1 : 2;
   ks.stage = s;
   ks.plm = (s == 2);
+  return ks;
+}
+
+bool can_prefetch(const pmhd_mesh* m) { return m->overlap && m->variant == 0 && !m->prof; }
+
+// Interior flux tiles of stage s on stream2, after the work already on the
+// main stream (the update that produced their input); the ghost exchange that
+// follows on the main stream runs concurrently (the tiles read no ghost data).
+int prefetch_stage(pmhd_mesh* m, int s, double dt) {
+  pmhd_ctx* ctx = m->ctx;
+  const KGeom& G = m->G;
+  const KStage ks = make_stage(G, s, dt);
+  CK(cudaEventRecord(m->ev_pre[0], ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->stream2, m->ev_pre[0], 0));
+  for (int dir = 0; dir < G.dim; ++dir)
+    launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], s, m->dred, 0, 1,
+                      G.ke - G.ks, ctx->stream2, 1);
+  CK(cudaEventRecord(m->ev_pre[1], ctx->stream2));
+  m->times.kernel_launches += G.dim;
+  m->prefetched = s;
+  m->prefetch_dt = dt;
+  CK(cudaGetLastError());
+  return PMHD_OK;
+}
+
+// Enqueue one VL2 stage (no synchronization unless profiling).
+// prefetch_next: enqueue the next stage's interior flux tiles (same dt) on
+// stream2 before this stage's exchange, so they overlap it.
+int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool prefetch_next = false) {
+  pmhd_ctx* ctx = m->ctx;
+  const KGeom& G = m->G;
+  const KStage ks = make_stage(G, s, dt);
   cudaStream_t st = ctx->stream;
+  // interior tiles of this stage already enqueued (with this dt)?
+  int flux_region = 0;
+  if (m->prefetched) {
+    if (m->prefetched == s && m->prefetch_dt == dt && can_prefetch(m)) flux_region = 2;
+    CK(cudaStreamWaitEvent(st, m->ev_pre[1], 0));  // (a stale prefetch must finish before it is redone)
+    m->prefetched = 0;
+  }
   // k-slab pipeline (fused variant, 3D, not profiling): the flux kernels of
   // slab q+1 run on the main stream while the update kernel of slab q (which
   // needs the faces of planes up to the first plane of slab q+1) runs on the
@@ -163,7 +206,8 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true) {
   // memory-bound update work.
   const int nk = G.ke - G.ks;
   int S = nk, nslab = 1;
-  if (m->variant == 0 && G.dim == 3 && !m->prof && m->slab_planes > 0 && nk >= 2 * m->slab_planes) {
+  if (m->variant == 0 && G.dim == 3 && !m->prof && m->slab_planes > 0 && nk >= 2 * m->slab_planes &&
+      flux_region == 0) {
     S = m->slab_planes;
     nslab = (nk + S - 1) / S;
   }
@@ -193,7 +237,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true) {
     for (int dir = 0; dir < G.dim; ++dir) {
       if (m->variant == 0)
         launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], s, m->dred, 0, 1,
-                          nk, st);
+                          nk, st, flux_region);
       else
         launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], st);
     }
@@ -207,6 +251,10 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true) {
       launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
     }
     rec(m, 4);
+    if (do_exchange && prefetch_next && s == 1 && can_prefetch(m)) {
+      int rc = prefetch_stage(m, 2, dt);
+      if (rc) return rc;
+    }
     if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st);
     rec(m, 5);
     m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim : 4 + G.dim) + (do_exchange ? G.dim : 0);
@@ -450,6 +498,12 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   const size_t nrows = size_t(G.nb) * 5 * (G.ke - G.ks) * (G.je - G.js);
   CK(cudaMalloc(&m->drows, nrows * sizeof(double)));
   for (auto& e : m->ev) CK(cudaEventCreate(&e));
+  for (auto& e : m->ev_pre) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // Overlap pays where the exchange is a real transfer (remote neighbours,
+  // NCCL); with all neighbours local the exchange kernels take ~3 % of a
+  // stage and splitting the flux launches costs more (measured -1.4 % at 256^3).
+  m->overlap = !m->all_local;
+  if (const char* ov = std::getenv("PMHD_OVERLAP")) m->overlap = std::atoi(ov) != 0;
   m->slab_ev.resize((G.ke - G.ks) / 8 + 2);
   for (auto& e : m->slab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -470,6 +524,7 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   cudaFreeHost(m->hred);
   for (auto& e : m->ev) if (e) cudaEventDestroy(e);
   for (auto& e : m->slab_ev) if (e) cudaEventDestroy(e);
+  for (auto& e : m->ev_pre) if (e) cudaEventDestroy(e);
   delete m;
   return PMHD_OK;
 }
@@ -587,7 +642,7 @@ int pmhd_gpu_vl2_step(pmhd_mesh* m, double dt, double* dt_next, pmhd_status* st)
   if (!m) return PMHD_ERR_INPUT;
   if (!m->all_local) return fail(m->ctx, PMHD_ERR_INPUT, "step needs all neighbours local");
   int rc = reset_red(m);
-  if (!rc) rc = enqueue_stage(m, 1, dt);
+  if (!rc) rc = enqueue_stage(m, 1, dt, true, true);  // + stage-2 interior tiles over the exchange
   if (!rc) rc = enqueue_stage(m, 2, dt);
   if (rc) return rc;
   return finish(m, 1, 2, dt_next, st);
@@ -713,10 +768,21 @@ int pmhd_gpu_stage_compute(pmhd_mesh* m, int stage, double dt, double* dt_next, 
     }
     return finish(m, 1, 2, dt_next, st);
   }
-  int rc = reset_red(m);
+  // a prefetched stage already accumulates into its reduction slot (reset by
+  // the previous stage_compute), so it is not reset again
+  int rc = (m->prefetched == stage) ? PMHD_OK : reset_red(m);
   if (!rc) rc = enqueue_stage(m, stage, dt, false);
   if (rc) return rc;
   return finish(m, stage, stage, stage == 2 ? dt_next : nullptr, st);
+}
+
+int pmhd_gpu_stage_prefetch(pmhd_mesh* m, int stage, double dt) {
+  if (!m) return PMHD_ERR_INPUT;
+  if (stage != 2) return fail(m->ctx, PMHD_ERR_INPUT, "only stage 2 can be prefetched");
+  if (!can_prefetch(m)) return PMHD_OK;  // stage_compute then runs every tile
+  pmhd_ctx* ctx = m->ctx;
+  if (m->prefetched) CK(cudaStreamWaitEvent(ctx->stream, m->ev_pre[1], 0));
+  return prefetch_stage(m, stage, dt);
 }
 
 int pmhd_gpu_drive_begin(pmhd_mesh* m, int nmode, const int* k, const double* c, const double* s,

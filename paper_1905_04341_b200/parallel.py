@@ -195,6 +195,7 @@ class DistributedVL2:
 
     def vl2_step(self, dt):
         _, s1 = self.e.stage_compute(1, dt)
+        self.e.stage_prefetch(2, dt)  # stage-2 interior tiles overlap the halo exchange
         self.exchange(half=1)
         dn, s2 = self.e.stage_compute(2, dt)
         self.exchange(half=0)
@@ -281,6 +282,7 @@ class LoopbackWorld:
     def vl2_step(self, dt):
         for e in self.engines:
             e.stage_compute(1, dt)
+            e.stage_prefetch(2, dt)
         self.exchange(half=1)
         dts = [e.stage_compute(2, dt)[0] for e in self.engines]
         self.exchange(half=0)

@@ -148,6 +148,10 @@ class GpuSolver:
         self._check(self.L.pmhd_gpu_stage_compute(self.mesh, s, dt, C.byref(dn), C.byref(st)), st)
         return dn.value, st
 
+    def stage_prefetch(self, s, dt):
+        """Stage s's interior flux tiles, overlapping the coming exchange."""
+        self._check(self.L.pmhd_gpu_stage_prefetch(self.mesh, s, dt))
+
     def exchange_dir(self, d, half):
         self._check(self.L.pmhd_gpu_exchange_dir(self.mesh, d, int(half)))
 

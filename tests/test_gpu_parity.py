@@ -209,6 +209,24 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
         assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
 
 
+@pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_4blk"])
+def test_overlap_prefetch_bitwise(gpu_available, case, monkeypatch):
+    """Stage-2 interior flux tiles enqueued on a second stream while the
+    stage-1 ghost exchange runs (PMHD_OVERLAP=1; on by default only with
+    remote neighbours) are bit-identical to the oracle."""
+    monkeypatch.setenv("PMHD_OVERLAP", "1")
+    kw, ncyc = CASES[case]
+    cfg = RunConfig(**kw)
+    o, g, _, (fo, fg), dts = run_pair(cfg, ncyc, parity=True)
+    assert fo == fg
+    for a, b in dts:
+        assert a == b
+    for gid in range(cfg.nblocks):
+        bo, bg = o.get_block(gid), g.get_block(gid)
+        for f in ("u", "b1f", "b2f", "b3f"):
+            assert np.array_equal(getattr(bo, f), getattr(bg, f)), (case, gid, f)
+
+
 @pytest.mark.parametrize("slab", [16, 32])
 @pytest.mark.parametrize("case", ["blast", "wave"])
 def test_kslab_pipeline_bitwise(gpu_available, slab, case, monkeypatch):
