@@ -143,6 +143,12 @@ class TorchDistTransport:
             for _, t, c in tmp:
                 t.copy_(c)
 
+    def allgather(self, obj):
+        """Python objects of every rank (rank order)."""
+        out = [None] * self.dist.get_world_size(self.group)
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
     def min(self, x, device=None):
         import torch
         t = torch.tensor([x], dtype=torch.float64, device=None if self.host_staging else device)
@@ -192,6 +198,14 @@ class DistributedVL2:
 
     def new_dt(self):
         return self.tr.min(self.e.new_dt(), self.device)
+
+    def kick(self, driver, event, de):
+        """One turbulence-driving event over all ranks (drive.py): per-block
+        sums all-gathered and combined in gid order, then the ghost exchange
+        (the engine's apply refreshed only ghosts with local sources)."""
+        scale = driver.kick(self.e, event, de, allgather=self.tr.allgather)
+        self.exchange(half=0)
+        return scale
 
     def vl2_step(self, dt):
         _, s1 = self.e.stage_compute(1, dt)

@@ -251,8 +251,18 @@ def test_kslab_pipeline_bitwise(gpu_available, slab, case, monkeypatch):
             assert np.array_equal(getattr(bo, f), getattr(bg, f)), (gid, f)
 
 
-@pytest.mark.parametrize("nranks,stream_ordered", [(2, False), (4, False), (2, True), (4, True)])
-def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered):
+MULTIRANK = {
+    "wave": dict(nx1=32, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, x2max=0.5, x3max=0.5, wave_n1=1,
+                 wave_n2=1, wave_amp=1e-3),
+    "blast": CASES["blast3d_8blk_floor"][0],
+    "ot2d": CASES["ot2d_4blk"][0],
+}
+
+
+@pytest.mark.parametrize("nranks,stream_ordered,case", [(2, False, "wave"), (4, False, "wave"),
+                                                        (2, True, "wave"), (4, True, "wave"),
+                                                        (2, True, "blast"), (4, True, "ot2d")])
+def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered, case):
     """The multi-rank data path (stage_compute + local sweeps + halo pack /
     unpack kernels + transport) with nranks rank-engines on ONE GPU, stepped in
     lockstep by the host (no kernel waits on another), is bit-identical to the
@@ -260,9 +270,7 @@ def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered):
     with the hand-over ordered by events between the engines' streams (what
     DistributedVL2 does with NCCL), i.e. no host synchronization in a stage."""
     from paper_1905_04341_b200.parallel import plan_for, LoopbackWorld
-    kw = dict(nx1=32, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, x2max=0.5, x3max=0.5, wave_n1=1,
-              wave_n2=1, wave_amp=1e-3)
-    cfg = RunConfig(**kw)
+    cfg = RunConfig(**MULTIRANK[case])
     plan = plan_for(cfg, nranks)
     engines = [GpuSolver(cfg, parity=True, gids=plan.local_gids(r)) for r in range(nranks)]
     for e in engines:

@@ -14,6 +14,8 @@ from paper_1905_04341_b200.parallel import partition, plan_for, HaloPlan
 CFG = dict(nx1=32, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, x2max=0.5, x3max=0.5, wave_n1=1,
            wave_n2=1, wave_amp=1e-3)
 CFG2D = dict(nx1=64, nx2=64, nx3=1, mb1=16, mb2=32, mb3=1, pgen="orszag_tang", cfl=0.4)
+CFGTURB = dict(nx1=16, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, pgen="turbulence", turb_drive=1,
+               turb_dedt=0.5, turb_every=2)
 
 
 def test_partition_bricks():
@@ -63,19 +65,30 @@ def _worker(rank, world, port, cfg_kw, ncyc, q):
         drv = DistributedVL2(eng, plan, rank, TorchDistTransport(dist))
         drv.exchange(half=0)
         dt = drv.new_dt()
-        for _ in range(ncyc):
-            dt, _ = drv.vl2_step(dt)
+        driver = None
+        if cfg.c.turb_drive:
+            from paper_1905_04341_b200.drive import TurbulenceDriver
+            driver = TurbulenceDriver(cfg)
+        acc, event = 0.0, 0
+        for n in range(ncyc):  # the loop of drive.run_driven, across ranks
+            dn, _ = drv.vl2_step(dt)
+            acc += dt
+            dt = dn
+            if driver is not None and (n + 1) % cfg.c.turb_every == 0:
+                drv.kick(driver, event, driver.energy(acc))
+                acc, event = 0.0, event + 1
+                dt = drv.new_dt()
         out = {gid: eng.get_block(gid).u for gid in eng.gids}
         q.put((rank, dt, out))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,cfg_kw", [(2, CFG), (4, CFG), (2, CFG2D)])
+@pytest.mark.parametrize("world,cfg_kw", [(2, CFG), (4, CFG), (2, CFG2D), (2, CFGTURB)])
 def test_gloo_sharded_equals_single_process(world, cfg_kw):
     import torch.multiprocessing as mp
     from oracle.binding import OracleSolver
-    ncyc = 3
+    ncyc = 4
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -89,9 +102,13 @@ def test_gloo_sharded_equals_single_process(world, cfg_kw):
     cfg = RunConfig(**cfg_kw)
     ref = OracleSolver(cfg, workers=4)
     ref.load_pgen()
-    dt = ref.new_dt()
-    for _ in range(ncyc):
-        dt, _ = ref.vl2_step(dt)
+    if cfg.c.turb_drive:
+        from paper_1905_04341_b200.drive import run_driven
+        _, dt, _ = run_driven(ref, cfg, ncyc)
+    else:
+        dt = ref.new_dt()
+        for _ in range(ncyc):
+            dt, _ = ref.vl2_step(dt)
     seen = set()
     for rank, dtr, blocks in results:
         assert dtr == dt
