@@ -13,7 +13,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -Xlinker -Bsymbolic -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Iinclude -I$(GPUSRC) \
             -Xptxas -warn-spills --expt-relaxed-constexpr
 HOSTFLAGS:= -std=c++20 -O2 -march=x86-64-v3 -fPIC -Wall -Wextra -Iinclude
-GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu $(GPUSRC)/kernels_flux.cu $(GPUSRC)/kernels_update.cu $(GPUSRC)/kernels_halo.cu $(GPUSRC)/kernels_drive.cu
+GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu $(GPUSRC)/kernels_flux.cu $(GPUSRC)/kernels_update.cu $(GPUSRC)/kernels_halo.cu $(GPUSRC)/kernels_drive.cu $(GPUSRC)/kernels_ctl.cu
 FASTDS   := -DPMHD_FAST_DIVSQRT
 GPU_DEPS := $(GPU_SRCS) $(wildcard $(GPUSRC)/*.cuh) include/pmhd_gpu.h Makefile
 

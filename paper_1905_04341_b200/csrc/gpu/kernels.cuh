@@ -57,11 +57,29 @@ struct DevRed {
 
 // Stage coefficients c_d = beta*dt/dx_d, computed on the host with the same
 // IEEE operations as the oracle.
+// Stage coefficients: by value, or (graph-replayed runs, kernel MODE 2) from
+// the device copy k_cycle_begin writes, so a captured cycle can be replayed.
+// skip != 0: the replayed cycle is past the end of the run; kernels return.
 struct KStage {
   double c1, c2, c3;
   double c1024[3];  // 1024 * dt / dx_d (contact-upwind weight scale)
   int in_sel, out_sel, stage, plm;  // base is always st[0]
+  int skip;
 };
+
+// Device-resident run control (graph-replayed pmhd_gpu_run): the cycle loop
+// of the ABI's run (dt cap to land on tlim) without a host
+// round trip per cycle.
+struct DevCtl {
+  double t, dt, tlim, h, cfl;
+  double dx[3];
+  int last, stop, cycles, ncycles;
+  unsigned long long floors, fallbacks;      // completed cycles
+  unsigned long long err_key, err_floors;    // failing cycle (stop with an error)
+  int err_stage, pad;
+};
+void launch_cycle_begin(DevCtl* ctl, KStage* dks, DevRed* red, cudaStream_t s);
+void launch_cycle_end(DevCtl* ctl, const KStage* dks, const DevRed* red, cudaStream_t s);
 
 // One halo slab message: per array v, its origin and extents (i, j, k) and its
 // offset in the contiguous buffer (off[8] = total doubles).
@@ -96,17 +114,21 @@ void launch_c2p_all(const DevBlock* blks, const KGeom& G, const KPhys& ph, int s
 void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel, int plm,
                  double c1024, cudaStream_t s);
 // region: 0 all tiles, 1 tiles clear of the ghost exchange, 2 the others
+// kd: nullptr (coefficients by value) or the device copy of a graph-replayed cycle
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
-                       int plm, double c1024, int stage, DevRed* red, int slab, int nslab, int S,
-                       cudaStream_t s, int region = 0);
+                       int plm, double c1024, const KStage* kd, int stage, DevRed* red, int slab,
+                       int nslab, int S, cudaStream_t s, int region = 0);
 void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s);
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
-                         DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s);
+                         const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s);
 void launch_update(const DevBlock* blks, const KGeom& G, const KStage& ks, cudaStream_t s);
 void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                     DevRed* red, int want_dt, cudaStream_t s);
-void launch_exchange(const DevBlock* blks, const KGeom& G, int sel, cudaStream_t s);
-void launch_exchange_dir(const DevBlock* blks, const KGeom& G, int sel, int dir, cudaStream_t s);
+// kd (optional): skip flag of a graph-replayed cycle
+void launch_exchange(const DevBlock* blks, const KGeom& G, int sel, cudaStream_t s,
+                     const KStage* kd = nullptr);
+void launch_exchange_dir(const DevBlock* blks, const KGeom& G, int sel, int dir, cudaStream_t s,
+                         const KStage* kd = nullptr);
 void launch_dt_from_state(const DevBlock* blks, const KGeom& G, const KPhys& ph, DevRed* red,
                           cudaStream_t s);
 void launch_divb(const DevBlock* blks, const KGeom& G, DevRed* red, cudaStream_t s);

@@ -66,11 +66,15 @@ __device__ __forceinline__ int rot_var(int n) {
   return V[DIR][n];
 }
 
-template <int DIR, int RS, bool PROF>
+// MODE: 0 product, 1 region profiling (phase clocks), 2 graph-replayed cycle
+// (coefficient and skip flag read from the device copy kd)
+template <int DIR, int RS, int MODE>
 __global__ void __launch_bounds__(NTHR, FluxMinB<RS>::value)
-k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024,
-             int stage, DevRed* red, int write_ec, int f_i0, int f_i1, int f_s0, int f_s1, int f_t0,
-             int f_t1, int ty0, int region) {
+k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024_arg,
+             const KStage* __restrict__ kd, int stage, DevRed* red, int write_ec, int f_i0, int f_i1,
+             int f_s0, int f_s1, int f_t0, int f_t1, int ty0, int region) {
+  constexpr bool PROF = (MODE == 1);
+  const int skip = (MODE == 2) ? kd->skip : 0;  // tested once the stencil loads are in flight
   using TS = TileShape<DIR>;
   __shared__ double sw[7][TS::NCELL];  // primitives; after phase 2: q - dq/2 (low-face value)
   __shared__ double sp[7][TS::NCELL];  // after phase 2: q + dq/2 (high-face value)
@@ -127,6 +131,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       ub[p][10] = __ldg(S[7] + id + G.sy);
     }
   }
+  if (MODE == 2 && skip) return;
 #pragma unroll
   for (int p = 0; p < TS::PER; ++p) {
     if (cid[p] < 0) continue;
@@ -209,6 +214,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 
   // ---- phase 3: two faces per thread ---------------------------------------
   const int fc = threadIdx.x % FX;
+  const double c1024 = (MODE == 2) ? kd->c1024[DIR] : c1024_arg;
   const double* const wsrc = plm ? &sp[0][0] : &sw[0][0];  // low-side cell's high-face value
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
@@ -267,8 +273,8 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 // up to ke) and x3 face planes [ks + q S, ...) (the last up to ke); S is a
 // multiple of the x3 tile's FS (16).  nslab = 1 is the whole block.
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
-                       int plm, double c1024, int stage, DevRed* red, int slab, int nslab, int S,
-                       cudaStream_t s, int region) {
+                       int plm, double c1024, const KStage* kd, int stage, DevRed* red, int slab,
+                       int nslab, int S, cudaStream_t s, int region) {
   const int d3 = (G.dim == 3) ? 1 : 0;
   // face ranges of the oracle: [lo, hi) per axis
   int i0, i1, j0, j1, k0, k1;
@@ -296,12 +302,15 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   const dim3 grid((i1 - i0 + FX - 1) / FX, ty1 - ty0, (nt1 - nt0) * G.nb);
 #define PMHD_FLUX_LAUNCH(D, R)                                                                      \
   do {                                                                                              \
-    if (ph.prof)                                                                                    \
-      k_flux_fused<D, R, true><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red,      \
-                                                     write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
+    if (kd)                                                                                         \
+      k_flux_fused<D, R, 2><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
+                                                  write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
+    else if (ph.prof)                                                                               \
+      k_flux_fused<D, R, 1><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
+                                                  write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
     else                                                                                            \
-      k_flux_fused<D, R, false><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, stage, red,     \
-                                                      write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
+      k_flux_fused<D, R, 0><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
+                                                  write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
   } while (0)
 #define PMHD_FLUX_DIRS(R)                          \
   do {                                             \

@@ -318,7 +318,8 @@ __global__ void k_row_sums(const DevBlock* __restrict__ blks, KGeom G, double* r
 
 // Exchange sweep in direction DIR (exchange_ghosts).
 template <int DIR>
-__global__ void k_exchange(const DevBlock* __restrict__ blks, KGeom G, int sel) {
+__global__ void k_exchange(const DevBlock* __restrict__ blks, KGeom G, int sel, const KStage* kd) {
+  if (kd && kd->skip) return;  // graph-replayed cycle past the end of the run
   const int v = blockIdx.z % kNState;
   const int b = blockIdx.z / kNState;
   const int l = blockIdx.y;  // layer slot in [0, 2 ng + 1)
@@ -392,20 +393,21 @@ void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const
   k_c2p_end<<<grid_for(bx, G.nb), tb(), 0, s>>>(blks, G, ph, ks, red, want_dt, bx);
 }
 
-void launch_exchange(const DevBlock* blks, const KGeom& G, int sel, cudaStream_t s) {
-  for (int dir = 0; dir < G.dim; ++dir) launch_exchange_dir(blks, G, sel, dir, s);
+void launch_exchange(const DevBlock* blks, const KGeom& G, int sel, cudaStream_t s, const KStage* kd) {
+  for (int dir = 0; dir < G.dim; ++dir) launch_exchange_dir(blks, G, sel, dir, s, kd);
 }
 
-void launch_exchange_dir(const DevBlock* blks, const KGeom& G, int sel, int dir, cudaStream_t s) {
+void launch_exchange_dir(const DevBlock* blks, const KGeom& G, int sel, int dir, cudaStream_t s,
+                         const KStage* kd) {
   {
     long long plane;
     if (dir == 0) plane = (long long)(G.n3 + 1) * (G.n2 + 1);
     else if (dir == 1) plane = (long long)(G.n3 + 1) * (G.n1 + 1);
     else plane = (long long)(G.n2 + 1) * (G.n1 + 1);
     const dim3 g((unsigned)((plane + 255) / 256), 2 * G.ng + 1, G.nb * kNState);
-    if (dir == 0) k_exchange<0><<<g, 256, 0, s>>>(blks, G, sel);
-    else if (dir == 1) k_exchange<1><<<g, 256, 0, s>>>(blks, G, sel);
-    else k_exchange<2><<<g, 256, 0, s>>>(blks, G, sel);
+    if (dir == 0) k_exchange<0><<<g, 256, 0, s>>>(blks, G, sel, kd);
+    else if (dir == 1) k_exchange<1><<<g, 256, 0, s>>>(blks, G, sel, kd);
+    else k_exchange<2><<<g, 256, 0, s>>>(blks, G, sel, kd);
   }
 }
 

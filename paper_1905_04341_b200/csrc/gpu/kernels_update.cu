@@ -49,10 +49,16 @@ struct UpdSmem {
   long long tph[3];             // profiling (thread 0): mark, EMF cycles, update cycles
 };
 
-template <int SEG, bool PROF>
+// MODE: 0 product, 1 region profiling, 2 graph-replayed cycle (stage from kd)
+template <int SEG, int MODE>
 __global__ void __launch_bounds__(UTHR, PMHD_UPDATE_MINB)
-k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, DevRed* red,
-               int want_dt, int kr0, int kr1) {
+k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_arg,
+               const KStage* __restrict__ kd, DevRed* red, int want_dt, int kr0, int kr1) {
+  // graph-replayed cycle past the end of the run: tested after the prologue's
+  // E loads are issued (before any global write)
+  constexpr bool PROF = (MODE == 1);
+  const int skip = (MODE == 2) ? kd->skip : 0;
+  const KStage ks = (MODE == 2) ? *kd : ks_arg;
   extern __shared__ __align__(16) unsigned char upd_smem[];
   UpdSmem& SM = *reinterpret_cast<UpdSmem*>(upd_smem);
   auto& ec = SM.ec;
@@ -150,6 +156,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
   if (d3) load_ec(kb - 1);
   load_ec(kb);
   __syncthreads();
+  if (MODE == 2 && skip) return;  // (uniform: every thread of every CTA)
   edge_emfs(kb, kb & 1);
   __syncthreads();
   face_b3(kb, kb & 1);
@@ -274,7 +281,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks, 
 }  // namespace
 
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
-                         DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s) {
+                         const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s) {
   // segment length: PMHD_UPDATE_SEG planes, or 4 / 1 when the mesh is too
   // small to fill ~2 waves of 148 SMs x 5 CTAs otherwise
   const int tiles = ((G.ie - G.is + UX - 1) / UX) * ((G.je - G.js + UY - 1) / UY) * G.nb;
@@ -285,18 +292,21 @@ void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, 
   const int nseg = (nk + seg - 1) / seg;
   const dim3 grid((G.ie - G.is + UX - 1) / UX, (G.je - G.js + UY - 1) / UY, nseg * G.nb);
   constexpr int smem = (int)sizeof(UpdSmem);
-#define PMHD_UPDATE_LAUNCH(SG)                                                                      \
-  do {                                                                                              \
-    static bool attr = false;                                                                       \
-    if (!attr) {                                                                                    \
-      cudaFuncSetAttribute(k_update_fused<SG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);  \
-      cudaFuncSetAttribute(k_update_fused<SG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-      attr = true;                                                                                  \
-    }                                                                                               \
-    if (ph.prof)                                                                                    \
-      k_update_fused<SG, true><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1);  \
-    else                                                                                            \
-      k_update_fused<SG, false><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, red, want_dt, kr0, kr1); \
+#define PMHD_UPDATE_LAUNCH(SG)                                                                          \
+  do {                                                                                                  \
+    static bool attr = false;                                                                           \
+    if (!attr) {                                                                                        \
+      cudaFuncSetAttribute(k_update_fused<SG, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
+      cudaFuncSetAttribute(k_update_fused<SG, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
+      cudaFuncSetAttribute(k_update_fused<SG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
+      attr = true;                                                                                      \
+    }                                                                                                   \
+    if (kd)                                                                                             \
+      k_update_fused<SG, 2><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1);      \
+    else if (ph.prof)                                                                                   \
+      k_update_fused<SG, 1><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1);      \
+    else                                                                                                \
+      k_update_fused<SG, 0><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1);      \
   } while (0)
   if (seg == PMHD_UPDATE_SEG) PMHD_UPDATE_LAUNCH(PMHD_UPDATE_SEG);
   else if (seg == 4) PMHD_UPDATE_LAUNCH(4);

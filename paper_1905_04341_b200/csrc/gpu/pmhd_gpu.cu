@@ -57,6 +57,13 @@ struct pmhd_mesh {
   // interior-tile prefetch (overlap of a stage's flux work with the previous
   // stage's ghost exchange): stage whose interior flux tiles are enqueued on
   // stream2, with the dt they used; ev_pre[0] = input ready, [1] = done
+  // device copies of the stage coefficients (dks[1], dks[2]) and the run
+  // control of a graph-replayed pmhd_gpu_run; graphs cached per table parity
+  KStage* dks = nullptr;
+  DevCtl* dctl = nullptr;
+  int parity = 0;                 // table flips mod 2 (hblk/dblk vs their alternates)
+  cudaGraphExec_t gexec[2] = {};  // two cycles each, starting from parity 0 / 1
+  bool graphs = true;             // PMHD_GRAPH=0 disables the graph-replayed run
   int prefetched = 0;
   double prefetch_dt = 0.0;
   cudaEvent_t ev_pre[2] = {};
@@ -159,6 +166,7 @@ KStage make_stage(const KGeom& G, int s, double dt) {
   ks.out_sel = (s == 1) ? 1 : 2;
   ks.stage = s;
   ks.plm = (s == 2);
+  ks.skip = 0;
   return ks;
 }
 
@@ -174,8 +182,8 @@ int prefetch_stage(pmhd_mesh* m, int s, double dt) {
   CK(cudaEventRecord(m->ev_pre[0], ctx->stream));
   CK(cudaStreamWaitEvent(ctx->stream2, m->ev_pre[0], 0));
   for (int dir = 0; dir < G.dim; ++dir)
-    launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], s, m->dred, 0, 1,
-                      G.ke - G.ks, ctx->stream2, 1);
+    launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], nullptr, s, m->dred, 0,
+                      1, G.ke - G.ks, ctx->stream2, 1);
   CK(cudaEventRecord(m->ev_pre[1], ctx->stream2));
   m->times.kernel_launches += G.dim;
   m->prefetched = s;
@@ -187,10 +195,14 @@ int prefetch_stage(pmhd_mesh* m, int s, double dt) {
 // Enqueue one VL2 stage (no synchronization unless profiling).
 // prefetch_next: enqueue the next stage's interior flux tiles (same dt) on
 // stream2 before this stage's exchange, so they overlap it.
-int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool prefetch_next = false) {
+// device_ks: the kernels read the coefficients (and the skip flag) from the
+// device copy k_cycle_begin writes in a captured cycle; else by value.
+int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool prefetch_next = false,
+                  bool device_ks = false) {
   pmhd_ctx* ctx = m->ctx;
   const KGeom& G = m->G;
   const KStage ks = make_stage(G, s, dt);
+  const KStage* kd = device_ks ? m->dks + s : nullptr;
   cudaStream_t st = ctx->stream;
   // interior tiles of this stage already enqueued (with this dt)?
   int flux_region = 0;
@@ -214,21 +226,21 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
   if (nslab > 1) {
     for (int q = 0; q < nslab; ++q) {
       for (int dir = 0; dir < G.dim; ++dir)
-        launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], s, m->dred, q,
+        launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], kd, s, m->dred, q,
                           nslab, S, st);
       CK(cudaEventRecord(m->slab_ev[q], st));
       if (q >= 1) {  // update slab q-1 once the flux kernels of slab q are done
         CK(cudaStreamWaitEvent(ctx->stream2, m->slab_ev[q], 0));
-        launch_update_fused(m->dblk, G, m->ph, ks, m->dred, s == 2, G.ks + (q - 1) * S,
+        launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks + (q - 1) * S,
                             G.ks + q * S, ctx->stream2);
       }
     }
     CK(cudaStreamWaitEvent(ctx->stream2, m->slab_ev[nslab - 1], 0));
-    launch_update_fused(m->dblk, G, m->ph, ks, m->dred, s == 2, G.ks + (nslab - 1) * S, G.ke,
+    launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks + (nslab - 1) * S, G.ke,
                         ctx->stream2);
     CK(cudaEventRecord(m->slab_ev[nslab], ctx->stream2));
     CK(cudaStreamWaitEvent(st, m->slab_ev[nslab], 0));
-    if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st);
+    if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st, kd);
     m->times.kernel_launches += nslab * (1 + G.dim) + (do_exchange ? G.dim : 0);
   } else {
     rec(m, 0);
@@ -236,7 +248,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     rec(m, 1);
     for (int dir = 0; dir < G.dim; ++dir) {
       if (m->variant == 0)
-        launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], s, m->dred, 0, 1,
+        launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], kd, s, m->dred, 0, 1,
                           nk, st, flux_region);
       else
         launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], st);
@@ -245,7 +257,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     if (m->variant == 1) launch_emf(m->dblk, G, m->ph, st);
     rec(m, 3);
     if (m->variant == 0) {
-      launch_update_fused(m->dblk, G, m->ph, ks, m->dred, s == 2, G.ks, G.ke, st);
+      launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks, G.ke, st);
     } else {
       launch_update(m->dblk, G, ks, st);
       launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
@@ -255,7 +267,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
       int rc = prefetch_stage(m, 2, dt);
       if (rc) return rc;
     }
-    if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st);
+    if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st, kd);
     rec(m, 5);
     m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim : 4 + G.dim) + (do_exchange ? G.dim : 0);
   }
@@ -263,6 +275,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
   if (s == 2) {  // u^{n+1} (st[2]) becomes the current state: flip the tables
     std::swap(m->hblk, m->hblk_alt);
     std::swap(m->dblk, m->dblk_alt);
+    m->parity ^= 1;
   }
   if (m->prof) {
     CK(cudaEventSynchronize(m->ev[5]));
@@ -494,6 +507,10 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   CK(cudaMemcpyAsync(m->dblk_alt, m->hblk_alt.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice,
                      ctx->stream));
   CK(cudaMalloc(&m->dred, 3 * sizeof(DevRed)));
+  CK(cudaMalloc(&m->dks, 3 * sizeof(KStage)));
+  CK(cudaMalloc(&m->dctl, sizeof(DevCtl)));
+  CK(cudaMemsetAsync(m->dks, 0, 3 * sizeof(KStage), ctx->stream));
+  if (const char* gr = std::getenv("PMHD_GRAPH")) m->graphs = std::atoi(gr) != 0;
   CK(cudaMallocHost(&m->hred, 3 * sizeof(DevRed)));
   const size_t nrows = size_t(G.nb) * 5 * (G.ke - G.ks) * (G.je - G.js);
   CK(cudaMalloc(&m->drows, nrows * sizeof(double)));
@@ -520,6 +537,9 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   cudaFree(m->dblk);
   cudaFree(m->dblk_alt);
   cudaFree(m->dred);
+  cudaFree(m->dks);
+  cudaFree(m->dctl);
+  for (auto& g : m->gexec) if (g) cudaGraphExecDestroy(g);
   cudaFree(m->drows);
   cudaFreeHost(m->hred);
   for (auto& e : m->ev) if (e) cudaEventDestroy(e);
@@ -648,6 +668,106 @@ int pmhd_gpu_vl2_step(pmhd_mesh* m, double dt, double* dt_next, pmhd_status* st)
   return finish(m, 1, 2, dt_next, st);
 }
 
+namespace {
+
+// The run loop with the cycle on the device: two cycles (one per table parity)
+// captured once into a CUDA graph and replayed, with k_cycle_begin/_end
+// carrying dt, t, the tlim cap, floors and the first error on the device; the
+// host synchronises every 32 cycles instead of every cycle.  Same arithmetic
+// as the host loop below, so the same bits.
+bool graph_run_ok(const pmhd_mesh* m) {
+  return m->graphs && m->variant == 0 && !m->prof && !m->async_ops && m->all_local && m->slab_planes == 0 &&
+         !m->overlap && !m->prefetched;
+}
+
+int capture_cycles(pmhd_mesh* m) {
+  pmhd_ctx* ctx = m->ctx;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = PMHD_OK;
+  for (int c = 0; c < 2 && !rc; ++c) {  // two cycles: the tables flip once per cycle
+    launch_cycle_begin(m->dctl, m->dks, m->dred, ctx->stream);
+    rc = enqueue_stage(m, 1, 0.0, true, false, true);
+    if (!rc) rc = enqueue_stage(m, 2, 0.0, true, false, true);
+    launch_cycle_end(m->dctl, m->dks, m->dred, ctx->stream);
+  }
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(ctx, PMHD_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&m->gexec[m->parity], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(ctx, PMHD_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  return PMHD_OK;
+}
+
+int graph_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int* cycles_done,
+              pmhd_status* st) {
+  pmhd_ctx* ctx = m->ctx;
+  const KGeom& G = m->G;
+  DevCtl c;
+  std::memset(&c, 0, sizeof(c));
+  c.t = *t;
+  c.dt = *dt;
+  c.tlim = tlim;
+  c.cfl = m->desc.cfl;
+  for (int a = 0; a < 3; ++a) c.dx[a] = G.dx[a];
+  c.ncycles = ncycles;
+  c.stop = ((ncycles >= 0 && ncycles <= 0) || (tlim > 0.0 && *t >= tlim)) ? 1 : 0;
+  c.err_key = ULLONG_MAX;
+  const int parity0 = m->parity;
+  if (!c.stop) {
+    if (!m->gexec[parity0]) {
+      int rc = capture_cycles(m);  // (capture leaves the tables as they were: two flips)
+      if (rc) return rc;
+    }
+    CK(cudaMemcpyAsync(m->dctl, &c, sizeof(c), cudaMemcpyHostToDevice, ctx->stream));
+    int launched = 0;
+    while (true) {
+      const int batch = 16;  // graph replays (2 cycles each) per host check
+      for (int q = 0; q < batch; ++q) CK(cudaGraphLaunch(m->gexec[parity0], ctx->stream));
+      launched += 2 * batch;
+      CK(cudaMemcpyAsync(&c, m->dctl, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (c.stop) break;
+      (void)launched;
+    }
+  }
+  // cycles that ran: the completed ones, plus the failing one (its stages ran
+  // and flipped the tables inside the graph)
+  const int ran = c.cycles + (c.err_key != ULLONG_MAX ? 1 : 0);
+  const long long per_cycle = 2 + 2 * (2 * G.dim + 1);
+  m->times.kernel_launches += per_cycle * ran;
+  if (ran & 1) {  // the state is in the other table after an odd number of cycles
+    std::swap(m->hblk, m->hblk_alt);
+    std::swap(m->dblk, m->dblk_alt);
+    m->parity ^= 1;
+  }
+  if (cycles_done) *cycles_done = c.cycles;
+  *t = c.t;
+  *dt = c.dt;
+  pmhd_status s{};
+  s.k = s.j = s.i = -1;
+  if (c.err_key != ULLONG_MAX) {
+    s.code = PMHD_ERR_UNPHYSICAL;
+    s.stage = c.err_stage;
+    s.floor_count = (long long)c.err_floors;
+    decode_key(G, c.err_key, &s);
+    if (st) *st = s;
+    ctx->err = "unphysical state in stage " + std::to_string(s.stage);
+    return PMHD_ERR_UNPHYSICAL;
+  }
+  if (st) {
+    s.code = PMHD_OK;
+    s.stage = 2;
+    s.floor_count = (long long)c.floors;
+    s.fallback_count = (long long)c.fallbacks;
+    *st = s;
+  }
+  return PMHD_OK;
+}
+
+}  // namespace
+
 int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int* cycles_done,
                  pmhd_status* st) {
   if (!m || !t || !dt) return PMHD_ERR_INPUT;
@@ -656,6 +776,7 @@ int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, 
     rc = pmhd_gpu_new_dt(m, dt, st);
     if (rc) return rc;
   }
+  if (graph_run_ok(m)) return graph_run(m, ncycles, tlim, t, dt, cycles_done, st);
   int n = 0;
   long long floors = 0, fallbacks = 0;
   while ((ncycles < 0 || n < ncycles) && (!(tlim > 0.0) || *t < tlim)) {

@@ -330,3 +330,46 @@ def test_driven_turbulence(gpu_available, parity):
                 assert np.array_equal(getattr(bo, f), getattr(bg, f)), (gid, f)
     else:
         assert scaled_diff(cfg, blocks(o, cfg), blocks(g, cfg)) <= TOL
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+@pytest.mark.parametrize("case,ncyc", [("blast3d_8blk_floor", 5), ("ot2d_4blk", 7), ("wave3d_roe", 3)])
+def test_run_loop_graph_replay_bitwise(gpu_available, graph, case, ncyc, monkeypatch):
+    """pmhd_gpu_run with the cycle captured as a CUDA graph and the dt / t /
+    floor bookkeeping on the device (PMHD_GRAPH=1, the default) and with the
+    host loop (0): both bit-identical to the oracle's run loop, odd cycle
+    counts included (the state ends in the other table), then more cycles
+    through vl2_step continue from the right table."""
+    monkeypatch.setenv("PMHD_GRAPH", graph)
+    cfg = RunConfig(**CASES[case][0])
+    o, g = OracleSolver(cfg, workers=8), GpuSolver(cfg, parity=True)
+    o.load_pgen()
+    g.load_pgen()
+    to, no, dto, fo = o.run(ncycles=ncyc)
+    tg, ng_, dtg, fg = g.run(ncycles=ncyc)
+    assert (to, no, dto, fo) == (tg, ng_, dtg, fg)
+    for _ in range(2):
+        dto, _ = o.vl2_step(dto)
+        dtg, _ = g.vl2_step(dtg)
+        assert dto == dtg
+    for gid in range(cfg.nblocks):
+        bo, bg = o.get_block(gid), g.get_block(gid)
+        for f in ("u", "b1f", "b2f", "b3f"):
+            assert np.array_equal(getattr(bo, f), getattr(bg, f)), (case, gid, f)
+
+
+def test_run_loop_graph_error(gpu_available):
+    """An unphysical state met inside a graph-replayed run is reported like
+    the host loop reports it (stage tag and global cell)."""
+    cfg = RunConfig(nx1=8, nx2=8, nx3=8, mb1=8, mb2=8, mb3=8, pgen="uniform", rho=1, p=1e-3,
+                    b1=0.0, b2=0.0, b3=0.0)
+    b = cfg.pgen_block(0)
+    b.u[4, 2 + 3, 2 + 1, 2 + 6] = -1.0
+    errs = []
+    for s in (OracleSolver(cfg), GpuSolver(cfg, parity=True)):
+        s.set_block(0, b)
+        s.exchange()
+        with pytest.raises(UnphysicalStateError) as ei:
+            s.run(ncycles=4, dt=1e-3)
+        errs.append((ei.value.stage_tag, ei.value.kk, ei.value.jj, ei.value.ii))
+    assert errs[0] == errs[1] == ("stage1", 3, 1, 6)
