@@ -74,7 +74,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
              const KStage* __restrict__ kd, int stage, DevRed* red, int write_ec, int f_i0, int f_i1,
              int f_s0, int f_s1, int f_t0, int f_t1, int ty0, int region) {
   constexpr bool PROF = (MODE == 1);
-  const int skip = (MODE == 2) ? kd->skip : 0;  // tested once the stencil loads are in flight
+  if (MODE == 2 && kd->skip) return;  // replayed cycle past the end of the run: no loads either
   using TS = TileShape<DIR>;
   __shared__ double sw[7][TS::NCELL];  // primitives; after phase 2: q - dq/2 (low-face value)
   __shared__ double sp[7][TS::NCELL];  // after phase 2: q + dq/2 (high-face value)
@@ -131,7 +131,6 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       ub[p][10] = __ldg(S[7] + id + G.sy);
     }
   }
-  if (MODE == 2 && skip) return;
 #pragma unroll
   for (int p = 0; p < TS::PER; ++p) {
     if (cid[p] < 0) continue;

@@ -57,7 +57,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
   // graph-replayed cycle past the end of the run: tested after the prologue's
   // E loads are issued (before any global write)
   constexpr bool PROF = (MODE == 1);
-  const int skip = (MODE == 2) ? kd->skip : 0;
+  if (MODE == 2 && kd->skip) return;  // replayed cycle past the end of the run
   const KStage ks = (MODE == 2) ? *kd : ks_arg;
   extern __shared__ __align__(16) unsigned char upd_smem[];
   UpdSmem& SM = *reinterpret_cast<UpdSmem*>(upd_smem);
@@ -156,7 +156,6 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
   if (d3) load_ec(kb - 1);
   load_ec(kb);
   __syncthreads();
-  if (MODE == 2 && skip) return;  // (uniform: every thread of every CTA)
   edge_emfs(kb, kb & 1);
   __syncthreads();
   face_b3(kb, kb & 1);

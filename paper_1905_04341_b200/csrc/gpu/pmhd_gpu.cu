@@ -63,7 +63,7 @@ struct pmhd_mesh {
   DevCtl* dctl = nullptr;
   int parity = 0;                 // table flips mod 2 (hblk/dblk vs their alternates)
   cudaGraphExec_t gexec[2] = {};  // two cycles each, starting from parity 0 / 1
-  bool graphs = true;             // PMHD_GRAPH=0 disables the graph-replayed run
+  int graphs = 2;                 // graph-replayed run: 2 auto (small meshes), PMHD_GRAPH=0/1
   int prefetched = 0;
   double prefetch_dt = 0.0;
   cudaEvent_t ev_pre[2] = {};
@@ -510,7 +510,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   CK(cudaMalloc(&m->dks, 3 * sizeof(KStage)));
   CK(cudaMalloc(&m->dctl, sizeof(DevCtl)));
   CK(cudaMemsetAsync(m->dks, 0, 3 * sizeof(KStage), ctx->stream));
-  if (const char* gr = std::getenv("PMHD_GRAPH")) m->graphs = std::atoi(gr) != 0;
+  if (const char* gr = std::getenv("PMHD_GRAPH")) m->graphs = std::atoi(gr) != 0 ? 1 : 0;
   CK(cudaMallocHost(&m->hred, 3 * sizeof(DevRed)));
   const size_t nrows = size_t(G.nb) * 5 * (G.ke - G.ks) * (G.je - G.js);
   CK(cudaMalloc(&m->drows, nrows * sizeof(double)));
@@ -676,8 +676,15 @@ namespace {
 // host synchronises every 32 cycles instead of every cycle.  Same arithmetic
 // as the host loop below, so the same bits.
 bool graph_run_ok(const pmhd_mesh* m) {
-  return m->graphs && m->variant == 0 && !m->prof && !m->async_ops && m->all_local && m->slab_planes == 0 &&
-         !m->overlap && !m->prefetched;
+  if (!(m->graphs != 0 && m->variant == 0 && !m->prof && !m->async_ops && m->all_local &&
+        m->slab_planes == 0 && !m->overlap && !m->prefetched))
+    return false;
+  if (m->graphs == 1) return true;  // PMHD_GRAPH=1
+  // auto: where the per-cycle host round trip is a visible share of a cycle
+  // (measured: 512^2 and 64^3 +13-15 %; 256^3 -1 %, the device-resident
+  // coefficients cost a little latency per CTA)
+  const long long cells = (long long)m->G.mb[0] * m->G.mb[1] * m->G.mb[2] * m->G.nb;
+  return cells < (1LL << 22);
 }
 
 int capture_cycles(pmhd_mesh* m) {
@@ -721,15 +728,22 @@ int graph_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int
       if (rc) return rc;
     }
     CK(cudaMemcpyAsync(m->dctl, &c, sizeof(c), cudaMemcpyHostToDevice, ctx->stream));
-    int launched = 0;
     while (true) {
-      const int batch = 16;  // graph replays (2 cycles each) per host check
-      for (int q = 0; q < batch; ++q) CK(cudaGraphLaunch(m->gexec[parity0], ctx->stream));
-      launched += 2 * batch;
+      // graph replays (2 cycles each) before the next host check: as many as
+      // the cycles left need (a replay past the end costs its skipped
+      // launches), at most 16
+      int pairs = 16;
+      if (ncycles >= 0) pairs = std::min(pairs, (ncycles - c.cycles + 1) / 2);
+      if (tlim > 0.0 && c.dt > 0.0) {
+        const double est = (tlim - c.t) / c.dt;  // cycles left at the current dt
+        if (est < 2.0 * pairs) pairs = std::max(1, (int)std::ceil(0.5 * est) + 1);
+        if (ncycles >= 0) pairs = std::min(pairs, std::max(1, (ncycles - c.cycles + 1) / 2));
+      }
+      pairs = std::max(1, pairs);
+      for (int q = 0; q < pairs; ++q) CK(cudaGraphLaunch(m->gexec[parity0], ctx->stream));
       CK(cudaMemcpyAsync(&c, m->dctl, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
       if (c.stop) break;
-      (void)launched;
     }
   }
   // cycles that ran: the completed ones, plus the failing one (its stages ran
