@@ -9,6 +9,7 @@
 #ifndef PMHD_KERNELS_CUH_
 #define PMHD_KERNELS_CUH_
 
+#include <cuda.h>  // CUtensorMap (type only; maps are encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 #include "physics.cuh"
@@ -119,8 +120,14 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
                        int plm, double c1024, const KStage* kd, int stage, DevRed* red, int slab,
                        int nslab, int S, cudaStream_t s, int region = 0);
 void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s);
+// ec_maps (optional, 3D meshes): per block, TMA tensor maps of its 3 cell-E
+// arrays (box = the update tile's E box) -- the kernel then streams its E
+// ring with TMA, one plane ahead.  Box extents: update_ec_box().
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
-                         const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s);
+                         const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s,
+                         const CUtensorMap* ec_maps = nullptr);
+void update_ec_box(int box[2]);
+bool update_uses_tma();  // built with PMHD_UPDATE_TMA
 void launch_update(const DevBlock* blks, const KGeom& G, const KStage& ks, cudaStream_t s);
 void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                     DevRed* red, int want_dt, cudaStream_t s);

@@ -24,6 +24,13 @@ namespace {
 #endif
 constexpr int UX = 32, UY = PMHD_UPDATE_UY, UTHR = UX * UY;
 constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0-1 .. j1)
+#ifndef PMHD_UPDATE_TMA
+// 1: stream the E ring with TMA one plane ahead (measured at 256^3: -2 %
+// against the plain loads -- the extra live state costs registers -- so off)
+#define PMHD_UPDATE_TMA 0
+#endif
+// E ring slot stride (doubles): 128 B aligned for TMA boxes, dense otherwise
+constexpr int ECS = PMHD_UPDATE_TMA ? ((EX * EY * 8 + 127) / 128) * 16 : EX * EY;
 #ifndef PMHD_UPDATE_MINB
 #define PMHD_UPDATE_MINB (1280 / (32 * PMHD_UPDATE_UY))  // 40 warps/SM of budget (48 regs)
 #endif
@@ -36,9 +43,40 @@ constexpr int EX = UX + 2, EY = UY + 2;  // Ec box extents (cells i0-1 .. i1, j0
 // recomputed: the cell-centred E ring holds planes k and k+1 (one new plane
 // loaded per step), E1 / E2 at k+1/2 become the k-1/2 values of the next
 // step, and so does the new b3 face at k+1.
+// ---- TMA + mbarrier (PTX) ----------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, unsigned long long* bar, int x,
+                                            int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Shared memory of one CTA (dynamic: > 48 KB for 32 x 16 tiles).
-struct UpdSmem {
-  double ec[3][2][EY][EX];      // cell-centred E: [component][k & 1][j][i]
+struct alignas(PMHD_UPDATE_TMA ? 128 : 16) UpdSmem {
+  // cell-centred E ring: [component][k & 1] boxes of EY x EX (one TMA box
+  // each; slots padded to 128 B multiples)
+  double ecbuf[3][2][ECS];
+  unsigned long long bar[2];    // TMA completion barriers, one per ring slot
   double e3s[UY + 1][UX + 1];   // E3 at (k, j-1/2, i-1/2)
   double e1s[2][UY + 1][UX];    // E1 at (k -/+ 1/2, j-1/2, i), slot by parity
   double e2s[2][UY][UX + 1];    // E2 at (k -/+ 1/2, j, i-1/2)
@@ -53,15 +91,22 @@ struct UpdSmem {
 template <int SEG, int MODE>
 __global__ void __launch_bounds__(UTHR, PMHD_UPDATE_MINB)
 k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_arg,
-               const KStage* __restrict__ kd, DevRed* red, int want_dt, int kr0, int kr1) {
+               const KStage* __restrict__ kd, DevRed* red, int want_dt, int kr0, int kr1,
+               const CUtensorMap* __restrict__ ec_maps) {
   // graph-replayed cycle past the end of the run: tested after the prologue's
   // E loads are issued (before any global write)
   constexpr bool PROF = (MODE == 1);
   if (MODE == 2 && kd->skip) return;  // replayed cycle past the end of the run
   const KStage ks = (MODE == 2) ? *kd : ks_arg;
   extern __shared__ __align__(16) unsigned char upd_smem[];
+  // (128 B alignment for the TMA boxes; the launch adds 128 bytes of slack)
+#if PMHD_UPDATE_TMA
+  UpdSmem& SM = *reinterpret_cast<UpdSmem*>((reinterpret_cast<uintptr_t>(upd_smem) + 127) &
+                                            ~uintptr_t(127));
+#else
   UpdSmem& SM = *reinterpret_cast<UpdSmem*>(upd_smem);
-  auto& ec = SM.ec;
+#endif
+  auto ec = [&](int c, int sl) { return reinterpret_cast<double(*)[EX]>(&SM.ecbuf[c][sl][0]); };
   auto& e3s = SM.e3s;
   auto& e1s = SM.e1s;
   auto& e2s = SM.e2s;
@@ -99,9 +144,9 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       const int c = q % EX, r = q / EX;
       if (c > nx + 1 || r > ny + 1) continue;
       const int id = G.idx(kk, j0 - 1 + r, i0 - 1 + c);
-      ec[0][sl][r][c] = __ldg(B.ec[0] + id);
-      ec[1][sl][r][c] = __ldg(B.ec[1] + id);
-      ec[2][sl][r][c] = __ldg(B.ec[2] + id);
+      ec(0, sl)[r][c] = __ldg(B.ec[0] + id);
+      ec(1, sl)[r][c] = __ldg(B.ec[1] + id);
+      ec(2, sl)[r][c] = __ldg(B.ec[2] + id);
     }
   };
   // E1 / E2 on the edge plane kk - 1/2 (3D; in 2D the face E of plane k)
@@ -116,8 +161,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       double e;
       if (d3) {
         e = corner_emf(mode, X2[5][id], X2[5][id - sy], X3[6][id], X3[6][id - sx], X2[7][id],
-                       X2[7][id - sy], X3[7][id], X3[7][id - sx], ec[0][pa][r + 1][c + 1],
-                       ec[0][pa][r][c + 1], ec[0][pm][r + 1][c + 1], ec[0][pm][r][c + 1]);
+                       X2[7][id - sy], X3[7][id], X3[7][id - sx], ec(0, pa)[r + 1][c + 1],
+                       ec(0, pa)[r][c + 1], ec(0, pm)[r + 1][c + 1], ec(0, pm)[r][c + 1]);
       } else {
         e = X2[5][id];
       }
@@ -131,8 +176,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       double e;
       if (d3) {
         e = corner_emf(mode, X3[5][id], X3[5][id - 1], X1[6][id], X1[6][id - sy], X3[7][id],
-                       X3[7][id - 1], X1[7][id], X1[7][id - sy], ec[1][pa][r + 1][c + 1],
-                       ec[1][pm][r + 1][c + 1], ec[1][pa][r + 1][c], ec[1][pm][r + 1][c]);
+                       X3[7][id - 1], X1[7][id], X1[7][id - sy], ec(1, pa)[r + 1][c + 1],
+                       ec(1, pm)[r + 1][c + 1], ec(1, pa)[r + 1][c], ec(1, pm)[r + 1][c]);
       } else {
         e = X1[6][id];
       }
@@ -152,12 +197,51 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
     }
   };
 
+  // TMA E ring (3D): thread 0 issues plane kk into its slot (one box per
+  // component); everyone waits on the slot's barrier before reading it.  A
+  // plane is issued one step ahead, as soon as its slot's previous plane has
+  // been read, so the E stream overlaps the CT / update phases.
+#if PMHD_UPDATE_TMA
+  const bool tma = (ec_maps != nullptr) && d3;
+#else
+  constexpr bool tma = false;
+#endif
+  unsigned eph = 0u;  // barrier phase bit of each ring slot (bit sl)
+  auto issue_ec = [&](int kk) {
+    if (tid == 0) {
+      const int sl = kk & 1;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads of the slot
+      mbar_expect_tx(&SM.bar[sl], 3u * EX * EY * 8u);
+      for (int c = 0; c < 3; ++c)  // the maps start at i = -1: cell i0-1 is x = i0
+        tma_load_3d(&SM.ecbuf[c][sl][0], ec_maps + 3 * b + c, &SM.bar[sl], i0, j0 - 1, kk);
+    }
+  };
+  auto wait_ec = [&](int kk) {
+    const int sl = kk & 1;
+    mbar_wait(&SM.bar[sl], (eph >> sl) & 1u);
+    eph ^= 1u << sl;
+  };
+
   // ---- prologue: Ec planes kb-1, kb and the edge EMFs at kb - 1/2 ----------
-  if (d3) load_ec(kb - 1);
-  load_ec(kb);
+  if (tma) {
+    if (tid == 0) {
+      mbar_init(&SM.bar[0], 1);
+      mbar_init(&SM.bar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    issue_ec(kb - 1);
+    issue_ec(kb);
+    wait_ec(kb - 1);
+    wait_ec(kb);
+  } else {
+    if (d3) load_ec(kb - 1);
+    load_ec(kb);
+  }
   __syncthreads();
   edge_emfs(kb, kb & 1);
   __syncthreads();
+  if (tma && kb + 1 <= kend) issue_ec(kb + 1);  // (slot of kb-1, read by the edge EMFs above)
   face_b3(kb, kb & 1);
 
   double tmin = 1.0e300;
@@ -165,7 +249,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
     const int lo = k & 1, hi = lo ^ 1;  // slots of k - 1/2 and k + 1/2
     if (PROF && tid == 0 && k > kb) { const long long t = clock64(); tph[2] += t - tph[0]; tph[0] = t; }
     // ---- A: the next Ec plane (slot of k-1, no longer needed) --------------
-    if (d3) load_ec(k + 1);
+    if (tma) wait_ec(k + 1);
+    else if (d3) load_ec(k + 1);
     __syncthreads();
     // ---- B: E3 at plane k, E1 / E2 at k + 1/2 -------------------------------
 #pragma unroll
@@ -175,12 +260,13 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       const int id = G.idx(k, j0 + r, i0 + c);
       const int ec_c = c + 1, ec_r = r + 1;
       e3s[r][c] = corner_emf(mode, X1[5][id], X1[5][id - sx], X2[6][id], X2[6][id - 1], X1[7][id],
-                             X1[7][id - sx], X2[7][id], X2[7][id - 1], ec[2][lo][ec_r][ec_c],
-                             ec[2][lo][ec_r][ec_c - 1], ec[2][lo][ec_r - 1][ec_c],
-                             ec[2][lo][ec_r - 1][ec_c - 1]);
+                             X1[7][id - sx], X2[7][id], X2[7][id - 1], ec(2, lo)[ec_r][ec_c],
+                             ec(2, lo)[ec_r][ec_c - 1], ec(2, lo)[ec_r - 1][ec_c],
+                             ec(2, lo)[ec_r - 1][ec_c - 1]);
     }
     edge_emfs(k + 1, hi);
     __syncthreads();
+    if (tma && k + 2 <= kend) issue_ec(k + 2);  // into slot lo: plane k was last read just above
     if (PROF && tid == 0) { const long long t = clock64(); tph[1] += t - tph[0]; tph[0] = t; }
     // ---- C: constrained-transport face update -------------------------------
     for (int q = tid; q < UY * (UX + 1); q += UTHR) {  // b1f, faces i0 .. i0+nx
@@ -279,8 +365,16 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
 
 }  // namespace
 
+void update_ec_box(int box[2]) {
+  box[0] = EX;
+  box[1] = EY;
+}
+
+bool update_uses_tma() { return PMHD_UPDATE_TMA != 0; }
+
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
-                         const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s) {
+                         const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s,
+                         const CUtensorMap* ec_maps) {
   // segment length: PMHD_UPDATE_SEG planes, or 4 / 1 when the mesh is too
   // small to fill ~2 waves of 148 SMs x 5 CTAs otherwise
   const int tiles = ((G.ie - G.is + UX - 1) / UX) * ((G.je - G.js + UY - 1) / UY) * G.nb;
@@ -290,7 +384,7 @@ void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, 
   const int seg = (fit >= PMHD_UPDATE_SEG) ? PMHD_UPDATE_SEG : (fit >= 4 ? 4 : 1);
   const int nseg = (nk + seg - 1) / seg;
   const dim3 grid((G.ie - G.is + UX - 1) / UX, (G.je - G.js + UY - 1) / UY, nseg * G.nb);
-  constexpr int smem = (int)sizeof(UpdSmem);
+  constexpr int smem = (int)sizeof(UpdSmem) + 128;  // + alignment slack
 #define PMHD_UPDATE_LAUNCH(SG)                                                                          \
   do {                                                                                                  \
     static bool attr = false;                                                                           \
@@ -301,11 +395,11 @@ void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, 
       attr = true;                                                                                      \
     }                                                                                                   \
     if (kd)                                                                                             \
-      k_update_fused<SG, 2><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1);      \
+      k_update_fused<SG, 2><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps);      \
     else if (ph.prof)                                                                                   \
-      k_update_fused<SG, 1><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1);      \
+      k_update_fused<SG, 1><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps);      \
     else                                                                                                \
-      k_update_fused<SG, 0><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1);      \
+      k_update_fused<SG, 0><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps);      \
   } while (0)
   if (seg == PMHD_UPDATE_SEG) PMHD_UPDATE_LAUNCH(PMHD_UPDATE_SEG);
   else if (seg == 4) PMHD_UPDATE_LAUNCH(4);

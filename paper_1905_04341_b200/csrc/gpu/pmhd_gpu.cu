@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -17,6 +18,8 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include <cudaTypedefs.h>
+
 #include "pmhd_gpu.h"
 
 using namespace pmhd_gpu;
@@ -59,6 +62,7 @@ struct pmhd_mesh {
   // stream2, with the dt they used; ev_pre[0] = input ready, [1] = done
   // device copies of the stage coefficients (dks[1], dks[2]) and the run
   // control of a graph-replayed pmhd_gpu_run; graphs cached per table parity
+  CUtensorMap* ec_maps = nullptr;  // TMA maps of the cell-E arrays (3 per block; nullptr: plain loads)
   KStage* dks = nullptr;
   DevCtl* dctl = nullptr;
   int parity = 0;                 // table flips mod 2 (hblk/dblk vs their alternates)
@@ -154,6 +158,42 @@ void rec(pmhd_mesh* m, int slot) {
   if (m->prof) cudaEventRecord(m->ev[slot], m->ctx->stream);
 }
 
+// TMA tensor maps of every block's 3 cell-E arrays for the update kernel's E
+// ring: 3D (i, j, k) over the pitched array, box = the kernel's E box.  The
+// map starts at element i = -1 so that its base is 16-byte aligned (rows are
+// aligned at i = is-1 = 1, i.e. i = -1 is on a 16 B boundary).
+int build_ec_maps(pmhd_mesh* m) {
+  if (!update_uses_tma()) return PMHD_OK;
+  if (const char* t = std::getenv("PMHD_TMA")) if (std::atoi(t) == 0) return PMHD_OK;
+  pmhd_ctx* ctx = m->ctx;
+  const KGeom& G = m->G;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return PMHD_OK;  // no driver entry point: the kernel uses plain loads
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  int box[2];
+  update_ec_box(box);
+  std::vector<CUtensorMap> maps(3 * size_t(G.nb));
+  for (int b = 0; b < G.nb; ++b)
+    for (int c = 0; c < 3; ++c) {
+      double* base = m->hblk[b].ec[c] - 1;
+      if (reinterpret_cast<uintptr_t>(base) % 16) return PMHD_OK;
+      const cuuint64_t dim[3] = {cuuint64_t(G.n1 + 1), cuuint64_t(G.n2), cuuint64_t(G.n3)};
+      const cuuint64_t stride[2] = {cuuint64_t(G.sx) * 8, cuuint64_t(G.sy) * 8};
+      const cuuint32_t bx[3] = {cuuint32_t(box[0]), cuuint32_t(box[1]), 1};
+      const cuuint32_t es[3] = {1, 1, 1};
+      const CUresult r = encode(&maps[3 * b + c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dim, stride, bx, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(ctx, PMHD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    }
+  CK(cudaMalloc(&m->ec_maps, maps.size() * sizeof(CUtensorMap)));
+  CK(cudaMemcpy(m->ec_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  return PMHD_OK;
+}
+
 KStage make_stage(const KGeom& G, int s, double dt) {
   const double beta = (s == 1) ? 0.5 : 1.0;
   const double bdt = beta * dt;
@@ -232,12 +272,12 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
       if (q >= 1) {  // update slab q-1 once the flux kernels of slab q are done
         CK(cudaStreamWaitEvent(ctx->stream2, m->slab_ev[q], 0));
         launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks + (q - 1) * S,
-                            G.ks + q * S, ctx->stream2);
+                            G.ks + q * S, ctx->stream2, m->ec_maps);
       }
     }
     CK(cudaStreamWaitEvent(ctx->stream2, m->slab_ev[nslab - 1], 0));
     launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks + (nslab - 1) * S, G.ke,
-                        ctx->stream2);
+                        ctx->stream2, m->ec_maps);
     CK(cudaEventRecord(m->slab_ev[nslab], ctx->stream2));
     CK(cudaStreamWaitEvent(st, m->slab_ev[nslab], 0));
     if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st, kd);
@@ -257,7 +297,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     if (m->variant == 1) launch_emf(m->dblk, G, m->ph, st);
     rec(m, 3);
     if (m->variant == 0) {
-      launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks, G.ke, st);
+      launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks, G.ke, st, m->ec_maps);
     } else {
       launch_update(m->dblk, G, ks, st);
       launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
@@ -508,6 +548,10 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
                      ctx->stream));
   CK(cudaMalloc(&m->dred, 3 * sizeof(DevRed)));
   CK(cudaMalloc(&m->dks, 3 * sizeof(KStage)));
+  if (G.dim == 3) {
+    int rc = build_ec_maps(m);
+    if (rc) { pmhd_gpu_mesh_destroy(m); return rc; }
+  }
   CK(cudaMalloc(&m->dctl, sizeof(DevCtl)));
   CK(cudaMemsetAsync(m->dks, 0, 3 * sizeof(KStage), ctx->stream));
   if (const char* gr = std::getenv("PMHD_GRAPH")) m->graphs = std::atoi(gr) != 0 ? 1 : 0;
@@ -538,6 +582,7 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   cudaFree(m->dblk_alt);
   cudaFree(m->dred);
   cudaFree(m->dks);
+  if (m->ec_maps) cudaFree(m->ec_maps);
   cudaFree(m->dctl);
   for (auto& g : m->gexec) if (g) cudaGraphExecDestroy(g);
   cudaFree(m->drows);

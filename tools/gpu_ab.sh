@@ -11,6 +11,7 @@ for v in "$@"; do
     sh_*) IFS=_ read -r _ a b c <<< "$v"; PMHD_ROW_SHIFT_ST=$a PMHD_ROW_SHIFT_FX=$b PMHD_ROW_SHIFT_EC=$c $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     shift*) PMHD_ROW_SHIFT=${v#shift} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     slab*) PMHD_SLAB_PLANES=${v#slab} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    notma) PMHD_TMA=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     nooverlap) PMHD_OVERLAP=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     hlle|roe) $B --riemann $v > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     *-hlle|*-roe) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_${v%-*}.so $B --riemann ${v##*-} > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
