@@ -387,12 +387,14 @@ void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, 
   constexpr int smem = (int)sizeof(UpdSmem) + 128;  // + alignment slack
 #define PMHD_UPDATE_LAUNCH(SG)                                                                          \
   do {                                                                                                  \
-    static bool attr = false;                                                                           \
-    if (!attr) {                                                                                        \
+    static unsigned long long attr_devs = 0; /* (per device: the attribute is per-device state) */    \
+    int dev = 0;                                                                                        \
+    cudaGetDevice(&dev);                                                                                \
+    if (!(attr_devs & (1ULL << (dev & 63)))) {                                                          \
       cudaFuncSetAttribute(k_update_fused<SG, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
       cudaFuncSetAttribute(k_update_fused<SG, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
       cudaFuncSetAttribute(k_update_fused<SG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
-      attr = true;                                                                                      \
+      attr_devs |= 1ULL << (dev & 63);                                                                  \
     }                                                                                                   \
     if (kd)                                                                                             \
       k_update_fused<SG, 2><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps);      \
