@@ -466,8 +466,10 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   if (n_local <= 0 || !gids) {
     for (int g = 0; g < ntot; ++g) m->gids.push_back(g);
   } else {
+    std::vector<char> seen(ntot, 0);
     for (int b = 0; b < n_local; ++b) {
       if (gids[b] < 0 || gids[b] >= ntot) { delete m; return fail(ctx, PMHD_ERR_CONFIG, "gid out of range"); }
+      if (seen[gids[b]]++) { delete m; return fail(ctx, PMHD_ERR_CONFIG, "duplicate gid"); }
       m->gids.push_back(gids[b]);
     }
   }
