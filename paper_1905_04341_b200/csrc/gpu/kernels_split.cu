@@ -317,37 +317,67 @@ __global__ void k_row_sums(const DevBlock* __restrict__ blks, KGeom G, double* r
 }
 
 // Exchange sweep in direction DIR (exchange_ghosts).
+// Layer slot l in [0, 2 ng + 1): l < ng lower ghosts (l <= ng for the normal
+// face array), the rest upper.  For x1 the layers of one row are a few
+// doubles apart, so one thread copies all of them (loads first: more bytes
+// in flight per thread on this latency-bound strided copy); x2 / x3 use one
+// thread per (row, layer).
+__device__ __forceinline__ bool exch_layer(const KGeom& G, const DevBlock& B, int DIR, int v, int l, int* q,
+                                           int* qs, int* nb) {
+  const int ng = G.ng, m = G.mb[DIR];
+  const int e = ng + m;
+  const bool normal = (v == 5 + DIR);
+  if (!normal) {
+    if (l < ng) { *q = l; *qs = l + m; *nb = B.nbr[DIR][0]; }
+    else if (l < 2 * ng) { *q = e + (l - ng); *qs = *q - m; *nb = B.nbr[DIR][1]; }
+    else return false;
+  } else {
+    if (l <= ng) { *q = l; *qs = l + m; *nb = B.nbr[DIR][0]; }
+    else { *q = e + 1 + (l - ng - 1); *qs = *q - m; *nb = B.nbr[DIR][1]; }
+  }
+  return *nb >= 0;  // remote neighbour: filled by halo unpack
+}
+
 template <int DIR>
 __global__ void k_exchange(const DevBlock* __restrict__ blks, KGeom G, int sel, const KStage* kd) {
   if (kd && kd->skip) return;  // graph-replayed cycle past the end of the run
   const int v = blockIdx.z % kNState;
   const int b = blockIdx.z / kNState;
-  const int l = blockIdx.y;  // layer slot in [0, 2 ng + 1)
   const int e1 = G.n1 + (v == 5), e2 = G.n2 + (v == 6), e3 = G.n3 + (v == 7);
   const int ta = (DIR == 2) ? e2 : e3;      // slow transverse extent
   const int tb = (DIR == 0) ? e2 : e1;      // fast transverse extent
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= (long long)ta * tb) return;
   const int a = (int)(p / tb), c = (int)(p % tb);
-  const int ng = G.ng, m = G.mb[DIR];
-  const int s = ng, e = ng + m;
-  const bool normal = (v == 5 + DIR);
-  int q, qs, nb;
-  if (!normal) {
-    if (l < ng) { q = l; qs = q + m; nb = blks[b].nbr[DIR][0]; }
-    else if (l < 2 * ng) { q = e + (l - ng); qs = q - m; nb = blks[b].nbr[DIR][1]; }
-    else return;
+  const DevBlock& B = blks[b];
+  auto at = [&](int qq) {
+    if (DIR == 0) return G.idx(a, c, qq);
+    if (DIR == 1) return G.idx(a, qq, c);
+    return G.idx(qq, a, c);
+  };
+  if (DIR == 0) {
+    constexpr int MAXL = 9;  // 2 ng + 1 for ng <= 4
+    double val[MAXL];
+    int dst[MAXL], nbs[MAXL];
+    const int nl = 2 * G.ng + 1;
+#pragma unroll
+    for (int l = 0; l < MAXL; ++l) {
+      nbs[l] = -1;
+      int q, qs, nb;
+      if (l < nl && exch_layer(G, B, DIR, v, l, &q, &qs, &nb)) {
+        val[l] = blks[nb].st[sel][v][at(qs)];
+        dst[l] = at(q);
+        nbs[l] = nb;
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < MAXL; ++l)
+      if (nbs[l] >= 0) B.st[sel][v][dst[l]] = val[l];
   } else {
-    if (l <= ng) { q = l; qs = q + m; nb = blks[b].nbr[DIR][0]; }
-    else { q = e + 1 + (l - ng - 1); qs = q - m; nb = blks[b].nbr[DIR][1]; }
+    int q, qs, nb;
+    if (!exch_layer(G, B, DIR, v, blockIdx.y, &q, &qs, &nb)) return;
+    B.st[sel][v][at(q)] = blks[nb].st[sel][v][at(qs)];
   }
-  (void)s;
-  if (nb < 0) return;  // remote neighbour: filled by halo unpack
-  long long dst, src;
-  if (DIR == 0) { dst = G.idx(a, c, q); src = G.idx(a, c, qs); }
-  else if (DIR == 1) { dst = G.idx(a, q, c); src = G.idx(a, qs, c); }
-  else { dst = G.idx(q, a, c); src = G.idx(qs, a, c); }
-  blks[b].st[sel][v][dst] = blks[nb].st[sel][v][src];
 }
 
 }  // namespace
@@ -404,7 +434,8 @@ void launch_exchange_dir(const DevBlock* blks, const KGeom& G, int sel, int dir,
     if (dir == 0) plane = (long long)(G.n3 + 1) * (G.n2 + 1);
     else if (dir == 1) plane = (long long)(G.n3 + 1) * (G.n1 + 1);
     else plane = (long long)(G.n2 + 1) * (G.n1 + 1);
-    const dim3 g((unsigned)((plane + 255) / 256), 2 * G.ng + 1, G.nb * kNState);
+    // (x1: one thread per row does every layer; ng <= 4 is validated)
+    const dim3 g((unsigned)((plane + 255) / 256), dir == 0 ? 1 : 2 * G.ng + 1, G.nb * kNState);
     if (dir == 0) k_exchange<0><<<g, 256, 0, s>>>(blks, G, sel, kd);
     else if (dir == 1) k_exchange<1><<<g, 256, 0, s>>>(blks, G, sel, kd);
     else k_exchange<2><<<g, 256, 0, s>>>(blks, G, sel, kd);

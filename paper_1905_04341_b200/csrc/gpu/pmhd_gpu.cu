@@ -101,7 +101,7 @@ int fail(pmhd_ctx* ctx, int code, const std::string& msg) {
 }
 
 std::string validate(const pmhd_mesh_desc& d) {
-  if (d.ng < 2) return "ng must be >= 2";
+  if (d.ng < 2 || d.ng > 4) return "ng must be in [2, 4]";
   for (int a = 0; a < 3; ++a) {
     if (d.nx[a] < 1 || d.mb[a] < 1) return "cell counts must be positive";
     if (d.nx[a] % d.mb[a] != 0) return "global cells not divisible by meshblock cells";

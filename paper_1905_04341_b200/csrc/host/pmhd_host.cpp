@@ -507,7 +507,7 @@ int pmhd_host_config_parse(const char* text, pmhd_run_config* c, int* err_line, 
 
 int pmhd_host_validate(const pmhd_run_config* c, char* err, int errlen) {
   const pmhd_mesh_desc& m = c->mesh;
-  if (m.ng < 2) { set_err(err, errlen, "ng must be >= 2"); return PMHD_ERR_CONFIG; }
+  if (m.ng < 2 || m.ng > 4) { set_err(err, errlen, "ng must be in [2, 4]"); return PMHD_ERR_CONFIG; }
   for (int a = 0; a < 3; ++a) {
     if (m.nx[a] < 1 || m.mb[a] < 1) { set_err(err, errlen, "cell counts must be positive"); return PMHD_ERR_CONFIG; }
     if (m.nx[a] % m.mb[a]) {
