@@ -373,3 +373,35 @@ def test_run_loop_graph_error(gpu_available):
             s.run(ncycles=4, dt=1e-3)
         errs.append((ei.value.stage_tag, ei.value.kk, ei.value.jj, ei.value.ii))
     assert errs[0] == errs[1] == ("stage1", 3, 1, 6)
+
+
+def test_gpu_restart_bitwise_continuous(gpu_available, tmp_path):
+    """PMHD1 snapshot / restart on the GPU path: 3 cycles,
+    snapshot, a fresh mesh restarted from the file, 3 more cycles == 6
+    uninterrupted cycles, bit for bit (parity build)."""
+    cfg = RunConfig(**CASES["blast3d_8blk_floor"][0])
+    ref = GpuSolver(cfg, parity=True)
+    ref.load_pgen()
+    dt = ref.new_dt()
+    dts = []
+    for _ in range(6):
+        dt, _ = ref.vl2_step(dt)
+        dts.append(dt)
+    a = GpuSolver(cfg, parity=True)
+    a.load_pgen()
+    dt = a.new_dt()
+    for _ in range(3):
+        dt, _ = a.vl2_step(dt)
+    p = tmp_path / "r.pmhd"
+    cfg.snapshot_write(p, [a.get_block(g) for g in range(cfg.nblocks)], 0.0)
+    del a
+    blocks, _ = cfg.snapshot_read(p)
+    b = GpuSolver(cfg, parity=True)
+    for g, blk in enumerate(blocks):
+        b.set_block(g, blk)
+    b.exchange()
+    for q in range(3):
+        dt, _ = b.vl2_step(dt)
+        assert dt == dts[3 + q]
+    for g in range(cfg.nblocks):
+        assert np.array_equal(ref.get_block(g).u, b.get_block(g).u), g
