@@ -1,5 +1,7 @@
+"""Graph-replayed vs host-loop pmhd_gpu_run at the bench size: same bits,
+and the wall time of each (python tools/graph_check.py [n])."""
 import os, sys, time, numpy as np
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
 from paper_1905_04341_b200.solver import GpuSolver
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
