@@ -27,6 +27,9 @@ namespace {
 #ifndef PMHD_FLUX_T_FX
 #define PMHD_FLUX_T_FX 16  // x2 / x3 tiles: faces along i
 #endif
+#ifndef PMHD_FLUX_STCS
+#define PMHD_FLUX_STCS 1  // streaming (evict-first) stores of the face data (+0.3 %)
+#endif
 #ifndef PMHD_FLUX_X1_FX
 #define PMHD_FLUX_X1_FX 32  // x1 tiles: faces along i
 #endif
@@ -245,6 +248,16 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     if (fb)
       atomicAdd(&red[stage].fallback_count, 1ULL);
     double* const* F = B.fx[DIR];
+#if PMHD_FLUX_STCS  // streaming stores: the face data is read back by the next kernel, not reused here
+    __stcs(F[0] + id, out[0]);
+    __stcs(F[rot_var<DIR>(1)] + id, out[1]);
+    __stcs(F[rot_var<DIR>(2)] + id, out[2]);
+    __stcs(F[rot_var<DIR>(3)] + id, out[3]);
+    __stcs(F[4] + id, out[4]);
+    __stcs(F[5] + id, out[5]);
+    __stcs(F[6] + id, out[6]);
+    __stcs(F[7] + id, out[7]);
+#else
     F[0][id] = out[0];
     F[rot_var<DIR>(1)][id] = out[1];
     F[rot_var<DIR>(2)][id] = out[2];
@@ -253,6 +266,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     F[5][id] = out[5];
     F[6][id] = out[6];
     F[7][id] = out[7];
+#endif
   }
   if (PROF) {
     __syncthreads();
