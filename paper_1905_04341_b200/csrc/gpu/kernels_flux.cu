@@ -30,6 +30,9 @@ namespace {
 #ifndef PMHD_FLUX_STCS
 #define PMHD_FLUX_STCS 1  // streaming (evict-first) stores of the face data (+0.3 %)
 #endif
+#ifndef PMHD_P1_BATCH
+#define PMHD_P1_BATCH 3  // stencil cells whose loads are batched per thread
+#endif
 #ifndef PMHD_FLUX_X1_FX
 #define PMHD_FLUX_X1_FX 32  // x1 tiles: faces along i
 #endif
@@ -108,43 +111,49 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   }
 
   // ---- phase 1: load + cons_to_prim of the stencil cells into smem --------
-  // All PER cells' loads are issued before any is consumed (memory-level
-  // parallelism: up to 3 x 11 loads in flight per thread).
-  double ub[TS::PER][11];
-  int cid[TS::PER];
+  // The loads of PMHD_P1_BATCH cells are issued before any is consumed
+  // (memory-level parallelism: up to BATCH x 11 loads in flight per thread).
+  constexpr int NB = (PMHD_P1_BATCH < TS::PER) ? PMHD_P1_BATCH : TS::PER;
 #pragma unroll
-  for (int p = 0; p < TS::PER; ++p) {
+  for (int p0 = 0; p0 < TS::PER; p0 += NB) {
+  double ub[NB][11];
+  int cid[NB];
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    const int p = p0 + q;
+    cid[q] = -1;
+    if (p >= TS::PER) continue;
     const int c = threadIdx.x + p * NTHR;
     const int col = c % TS::NCOL, row = c / TS::NCOL;
     int i, j, k;
     if (DIR == 0) { i = fi0 - 2 + col; j = fs0 + row; k = t3; }
     else if (DIR == 1) { i = fi0 + col; j = fs0 - 2 + row; k = t3; }
     else { i = fi0 + col; k = fs0 - 2 + row; j = t3; }
-    cid[p] = -1;
     if (c < TS::NCELL && i >= 0 && i < G.n1 && j >= 0 && j < G.n2 && k >= 0 && k < G.n3) {
       const int id = G.idx(k, j, i);
-      cid[p] = id;
+      cid[q] = id;
 #pragma unroll
-      for (int v = 0; v < 5; ++v) ub[p][v] = __ldg(S[v] + id);
-      ub[p][5] = __ldg(S[5] + id);
-      ub[p][6] = __ldg(S[5] + id + 1);
-      ub[p][7] = __ldg(S[6] + id);
-      ub[p][8] = __ldg(S[6] + id + G.sx);
-      ub[p][9] = __ldg(S[7] + id);
-      ub[p][10] = __ldg(S[7] + id + G.sy);
+      for (int v = 0; v < 5; ++v) ub[q][v] = __ldg(S[v] + id);
+      ub[q][5] = __ldg(S[5] + id);
+      ub[q][6] = __ldg(S[5] + id + 1);
+      ub[q][7] = __ldg(S[6] + id);
+      ub[q][8] = __ldg(S[6] + id + G.sx);
+      ub[q][9] = __ldg(S[7] + id);
+      ub[q][10] = __ldg(S[7] + id + G.sy);
     }
   }
 #pragma unroll
-  for (int p = 0; p < TS::PER; ++p) {
-    if (cid[p] < 0) continue;
+  for (int q = 0; q < NB; ++q) {
+    if (cid[q] < 0) continue;
+    const int p = p0 + q;
     const int c = threadIdx.x + p * NTHR;
-    const int id = cid[p];
+    const int id = cid[q];
     double u[5], bc[3], w[8];
 #pragma unroll
-    for (int v = 0; v < 5; ++v) u[v] = ub[p][v];
-    bc[0] = 0.5 * (ub[p][5] + ub[p][6]);
-    bc[1] = 0.5 * (ub[p][7] + ub[p][8]);
-    bc[2] = 0.5 * (ub[p][9] + ub[p][10]);
+    for (int v = 0; v < 5; ++v) u[v] = ub[q][v];
+    bc[0] = 0.5 * (ub[q][5] + ub[q][6]);
+    bc[1] = 0.5 * (ub[q][7] + ub[q][8]);
+    bc[2] = 0.5 * (ub[q][9] + ub[q][10]);
     const int fl = cons_to_prim(u, bc, ph, w, false);
     // (k, j, i) of the cell from its tile position
     const int col = c % TS::NCOL, row = c / TS::NCOL;
@@ -171,6 +180,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     }
 #pragma unroll
     for (int n = 0; n < 7; ++n) sw[n][c] = w[rot_var<DIR>(n)];
+  }
   }
   __syncthreads();
   if (PROF && threadIdx.x == 0) tph[1] = clock64();
