@@ -27,6 +27,7 @@ cfg = bench.make_config(n, ranks)  # (2n) x n x n, one block per rank
 plan = plan_for(cfg, ranks)
 g = GpuSolver(cfg, gids=plan.local_gids(0))
 g.load_pgen(exchange=False)
+g.set_async(True)  # stream-ordered calls (as over NCCL): the events time the kernels, not host syncs
 stream = torch.cuda.ExternalStream(g.stream_handle)
 sends, recvs = plan.messages(0, 0)
 bufs = [(gid, side, g.alloc_halo(g.halo_count(0, 1 - side))) for _, _, gid, side in sends]
