@@ -35,6 +35,10 @@ CASES = {
                         wave_n1=1, wave_n2=1, wave_amp=1e-3, riemann="roe"), 4),
     "ot2d_roe": (dict(nx1=64, nx2=64, nx3=1, mb1=32, mb2=64, mb3=1, pgen="orszag_tang", cfl=0.4,
                       riemann="roe"), 20),
+    # a larger shock problem: 64^3 blast in 8 blocks, floors active
+    "blast3d_64_floor": (dict(nx1=64, nx2=64, nx3=64, mb1=32, mb2=32, mb3=32, x1min=-0.5, x1max=0.5,
+                              x2min=-0.5, x2max=0.5, x3min=-0.5, x3max=0.5, pgen="blast",
+                              eos_mode="floor", blast_r=0.1), 5),
 }
 
 
