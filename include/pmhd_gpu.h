@@ -190,6 +190,22 @@ int pmhd_gpu_halo_count(const pmhd_mesh* mesh, int dir, int side, long long* n);
 int pmhd_gpu_halo_pack(pmhd_mesh* mesh, int gid, int dir, int side, int half, double* dev_buf);
 /* ghosts of block gid on `side`, from the neighbour's pack(..., 1 - side) */
 int pmhd_gpu_halo_unpack(pmhd_mesh* mesh, int gid, int dir, int side, int half, const double* dev_buf);
+/* Peer-memory halo (one node, NVLink / NVSwitch): instead of pack -> transport
+ * -> unpack, pmhd_gpu_exchange_dir reads a remote neighbour's boundary
+ * layers straight from its memory.  Every rank exports its state slab
+ * (pmhd_gpu_slab: base + CUDA IPC handle, 64 bytes), maps the others'
+ * (pmhd_gpu_ipc_open) and calls pmhd_gpu_peer_attach with the owner of every
+ * gid and each rank's mapped base (NULL: no mapping, that rank's faces keep
+ * using halo pack / unpack; a rank's own entry is ignored).  Ranks must have
+ * created their meshes with their gids in ascending order.  Ordering is the
+ * caller's: before exchange_dir(d) on any rank, every rank must have finished
+ * the stage (d = x1) or its exchange_dir(d-1) -- a barrier per direction
+ * (DistributedVL2 uses a stream-ordered NCCL all-reduce of one int). */
+int pmhd_gpu_slab(const pmhd_mesh* mesh, void** base, void* ipc_handle /* 64 bytes or NULL */);
+int pmhd_gpu_ipc_open(pmhd_ctx* ctx, const void* ipc_handle, void** base);
+int pmhd_gpu_ipc_close(pmhd_ctx* ctx, void* base);
+int pmhd_gpu_peer_attach(pmhd_mesh* mesh, int nranks, const int* owner_of_gid, void* const* rank_base);
+
 /* Stream-ordered multi-rank mode (on != 0): exchange_dir / halo_pack /
  * halo_unpack return as soon as their kernels are enqueued on
  * pmhd_gpu_stream(ctx), and stage_compute(1) returns without synchronizing

@@ -41,6 +41,12 @@ struct DevBlock {
                            // kernels; aliases e[], which they do not use)
   int c[3];                // block coordinates
   int nbr[3][2];           // local index of the lower / upper neighbour
+  // peer-memory halo (pmhd_gpu_peer_attach): this block's base in its slab
+  // and, for a neighbour owned by another rank on the node, that block's base
+  // as mapped into this process (CUDA IPC over NVLink); an array of the
+  // neighbour is at rbase + (own array - base) (same layout on every rank)
+  const char* base;
+  const char* rbase[3][2];
 };
 
 // Device-side reduction slots: red[0] = init / dt, red[1..2] = stage 1..2.

@@ -323,19 +323,31 @@ __global__ void k_row_sums(const DevBlock* __restrict__ blks, KGeom G, double* r
 // in flight per thread on this latency-bound strided copy); x2 / x3 use one
 // thread per (row, layer).
 __device__ __forceinline__ bool exch_layer(const KGeom& G, const DevBlock& B, int DIR, int v, int l, int* q,
-                                           int* qs, int* nb) {
+                                           int* qs, int* nb, int* side) {
   const int ng = G.ng, m = G.mb[DIR];
   const int e = ng + m;
   const bool normal = (v == 5 + DIR);
   if (!normal) {
-    if (l < ng) { *q = l; *qs = l + m; *nb = B.nbr[DIR][0]; }
-    else if (l < 2 * ng) { *q = e + (l - ng); *qs = *q - m; *nb = B.nbr[DIR][1]; }
+    if (l < ng) { *q = l; *qs = l + m; *side = 0; }
+    else if (l < 2 * ng) { *q = e + (l - ng); *qs = *q - m; *side = 1; }
     else return false;
   } else {
-    if (l <= ng) { *q = l; *qs = l + m; *nb = B.nbr[DIR][0]; }
-    else { *q = e + 1 + (l - ng - 1); *qs = *q - m; *nb = B.nbr[DIR][1]; }
+    if (l <= ng) { *q = l; *qs = l + m; *side = 0; }
+    else { *q = e + 1 + (l - ng - 1); *qs = *q - m; *side = 1; }
   }
-  return *nb >= 0;  // remote neighbour: filled by halo unpack
+  *nb = B.nbr[DIR][*side];
+  // remote neighbour: read over peer memory if attached, else the halo
+  // unpack fills it
+  return *nb >= 0 || B.rbase[DIR][*side] != nullptr;
+}
+
+// source array of the copy: the local neighbour's, or the remote one's
+// (same offset from its block base)
+__device__ __forceinline__ const double* exch_src(const DevBlock* blks, const DevBlock& B, int DIR, int side,
+                                                  int nb, int sel, int v) {
+  if (nb >= 0) return blks[nb].st[sel][v];
+  const char* own = reinterpret_cast<const char*>(B.st[sel][v]);
+  return reinterpret_cast<const double*>(B.rbase[DIR][side] + (own - B.base));
 }
 
 template <int DIR>
@@ -362,21 +374,21 @@ __global__ void k_exchange(const DevBlock* __restrict__ blks, KGeom G, int sel, 
     const int nl = 2 * G.ng + 1;
 #pragma unroll
     for (int l = 0; l < MAXL; ++l) {
-      nbs[l] = -1;
-      int q, qs, nb;
-      if (l < nl && exch_layer(G, B, DIR, v, l, &q, &qs, &nb)) {
-        val[l] = blks[nb].st[sel][v][at(qs)];
+      nbs[l] = 0;
+      int q, qs, nb, side;
+      if (l < nl && exch_layer(G, B, DIR, v, l, &q, &qs, &nb, &side)) {
+        val[l] = exch_src(blks, B, DIR, side, nb, sel, v)[at(qs)];
         dst[l] = at(q);
-        nbs[l] = nb;
+        nbs[l] = 1;
       }
     }
 #pragma unroll
     for (int l = 0; l < MAXL; ++l)
-      if (nbs[l] >= 0) B.st[sel][v][dst[l]] = val[l];
+      if (nbs[l]) B.st[sel][v][dst[l]] = val[l];
   } else {
-    int q, qs, nb;
-    if (!exch_layer(G, B, DIR, v, blockIdx.y, &q, &qs, &nb)) return;
-    B.st[sel][v][at(q)] = blks[nb].st[sel][v][at(qs)];
+    int q, qs, nb, side;
+    if (!exch_layer(G, B, DIR, v, blockIdx.y, &q, &qs, &nb, &side)) return;
+    B.st[sel][v][at(q)] = exch_src(blks, B, DIR, side, nb, sel, v)[at(qs)];
   }
 }
 

@@ -51,6 +51,7 @@ struct pmhd_mesh {
   DevBlock* dblk_alt = nullptr;
   double* slab = nullptr;
   size_t arr_elems = 0;
+  size_t per_block = 0;            // doubles per block in the slab
   DevRed* dred = nullptr;         // 3 slots
   DevRed* hred = nullptr;         // pinned mirror
   double* drows = nullptr;
@@ -492,6 +493,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   const size_t arr = size_t(G.n3 + 1) * size_t(G.sy) + 64;
   m->arr_elems = arr;
   const size_t per_block = 59 * arr;
+  m->per_block = per_block;
   const size_t bytes = per_block * G.nb * sizeof(double);
   if (cudaMalloc(&m->slab, bytes) != cudaSuccess) {
     delete m;
@@ -515,6 +517,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   const int sh_ec = shift_env("PMHD_ROW_SHIFT_EC", shift_env("PMHD_ROW_SHIFT", a1));
   for (int b = 0; b < G.nb; ++b) {
     double* p = m->slab + size_t(b) * per_block + 32;
+    m->hblk[b].base = reinterpret_cast<const char*>(m->slab + size_t(b) * per_block);
     DevBlock& B = m->hblk[b];
     auto take = [&](int sh) { double* q = p - sh; p += arr; return q; };
     for (int s = 0; s < 3; ++s)
@@ -1029,6 +1032,72 @@ int pmhd_gpu_drive_apply(pmhd_mesh* m, const double* mean, double scale) {
   m->times.kernel_launches += 1 + m->G.dim;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->stream));
+  return PMHD_OK;
+}
+
+int pmhd_gpu_slab(const pmhd_mesh* m, void** base, void* ipc_handle) {
+  if (!m || !base) return PMHD_ERR_INPUT;
+  *base = m->slab;
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    pmhd_ctx* ctx = m->ctx;
+    CK(cudaIpcGetMemHandle(&h, m->slab));
+    std::memcpy(ipc_handle, &h, sizeof(h));
+  }
+  return PMHD_OK;
+}
+
+int pmhd_gpu_ipc_open(pmhd_ctx* ctx, const void* ipc_handle, void** base) {
+  if (!ctx || !ipc_handle || !base) return PMHD_ERR_INPUT;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, ipc_handle, sizeof(h));
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+  return PMHD_OK;
+}
+
+int pmhd_gpu_ipc_close(pmhd_ctx* ctx, void* base) {
+  if (!ctx || !base) return PMHD_ERR_INPUT;
+  CK(cudaIpcCloseMemHandle(base));
+  return PMHD_OK;
+}
+
+int pmhd_gpu_peer_attach(pmhd_mesh* m, int nranks, const int* owner_of_gid, void* const* rank_base) {
+  if (!m || nranks < 1 || !owner_of_gid || !rank_base) return PMHD_ERR_INPUT;
+  pmhd_ctx* ctx = m->ctx;
+  const KGeom& G = m->G;
+  const pmhd_mesh_desc& d = m->desc;
+  const int nb[3] = {d.nx[0] / d.mb[0], d.nx[1] / d.mb[1], d.nx[2] / d.mb[2]};
+  const int ntot = nb[0] * nb[1] * nb[2];
+  for (size_t b = 1; b < m->gids.size(); ++b)
+    if (m->gids[b] < m->gids[b - 1]) return fail(ctx, PMHD_ERR_INPUT, "peer_attach needs gids in ascending order");
+  // a rank's blocks sit in its slab in ascending gid order
+  std::vector<int> slot(ntot, -1), count(nranks, 0);
+  for (int g = 0; g < ntot; ++g) {
+    const int r = owner_of_gid[g];
+    if (r < 0 || r >= nranks) return fail(ctx, PMHD_ERR_INPUT, "owner out of range");
+    slot[g] = count[r]++;
+  }
+  for (std::vector<DevBlock>* tab : {&m->hblk, &m->hblk_alt})
+    for (int b = 0; b < G.nb; ++b) {
+      DevBlock& B = (*tab)[b];
+      const int gid = m->gids[b];
+      const int c0[3] = {gid % nb[0], (gid / nb[0]) % nb[1], gid / (nb[0] * nb[1])};
+      for (int a = 0; a < 3; ++a)
+        for (int side = 0; side < 2; ++side) {
+          B.rbase[a][side] = nullptr;
+          if (a >= G.dim || B.nbr[a][side] >= 0) continue;  // local neighbour
+          int c[3] = {c0[0], c0[1], c0[2]};
+          c[a] = (c[a] + (side ? 1 : -1) + nb[a]) % nb[a];
+          const int ng = (c[2] * nb[1] + c[1]) * nb[0] + c[0];
+          const char* rb = static_cast<const char*>(rank_base[owner_of_gid[ng]]);
+          if (!rb) continue;  // no mapping: halo pack / unpack serves this face
+          B.rbase[a][side] = rb + size_t(slot[ng]) * m->per_block * sizeof(double);
+        }
+    }
+  CK(cudaMemcpy(m->dblk, m->hblk.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m->dblk_alt, m->hblk_alt.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice));
+  for (auto& g : m->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
   return PMHD_OK;
 }
 

@@ -187,6 +187,7 @@ GPU_SYMBOLS = [
     "pmhd_gpu_build_info", "pmhd_gpu_stream", "pmhd_gpu_stage_compute", "pmhd_gpu_exchange_dir",
     "pmhd_gpu_halo_count", "pmhd_gpu_halo_pack", "pmhd_gpu_halo_unpack", "pmhd_gpu_set_async",
     "pmhd_gpu_drive_begin", "pmhd_gpu_drive_energy", "pmhd_gpu_drive_apply", "pmhd_gpu_stage_prefetch",
+    "pmhd_gpu_slab", "pmhd_gpu_ipc_open", "pmhd_gpu_ipc_close", "pmhd_gpu_peer_attach",
 ]
 
 
@@ -233,6 +234,10 @@ def gpu_lib(parity: bool = False) -> C.CDLL:
         L.pmhd_gpu_halo_unpack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.pmhd_gpu_set_async.argtypes = [C.c_void_p, C.c_int]
         L.pmhd_gpu_stage_prefetch.argtypes = [C.c_void_p, C.c_int, C.c_double]
+        L.pmhd_gpu_slab.argtypes = [C.c_void_p, _P(C.c_void_p), C.c_void_p]
+        L.pmhd_gpu_ipc_open.argtypes = [C.c_void_p, C.c_void_p, _P(C.c_void_p)]
+        L.pmhd_gpu_ipc_close.argtypes = [C.c_void_p, C.c_void_p]
+        L.pmhd_gpu_peer_attach.argtypes = [C.c_void_p, C.c_int, _ip, _P(C.c_void_p)]
         L.pmhd_gpu_drive_begin.argtypes = [C.c_void_p, C.c_int, _ip, _dp, _dp, _P(_dp), _P(_dp), _dp]
         L.pmhd_gpu_drive_energy.argtypes = [C.c_void_p, _dp, _dp]
         L.pmhd_gpu_drive_apply.argtypes = [C.c_void_p, _dp, C.c_double]

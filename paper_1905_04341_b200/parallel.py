@@ -143,6 +143,20 @@ class TorchDistTransport:
             for _, t, c in tmp:
                 t.copy_(c)
 
+    def barrier(self, stream=None):
+        """All ranks reached this point.  With a stream (stream-ordered NCCL):
+        a one-int all-reduce ordered on it -- work enqueued after it on that
+        stream starts only once every rank's earlier work on its stream is
+        done; the host does not wait."""
+        if stream is not None and self.stream_ordered:
+            import torch
+            with torch.cuda.stream(stream):
+                if not hasattr(self, "_flag"):
+                    self._flag = torch.zeros(1, dtype=torch.int32, device=torch.cuda.current_device())
+                self.dist.all_reduce(self._flag, group=self.group)
+        else:
+            self.dist.barrier(group=self.group)
+
     def allgather(self, obj):
         """Python objects of every rank (rank order)."""
         out = [None] * self.dist.get_world_size(self.group)
@@ -176,6 +190,15 @@ class DistributedVL2:
             for peer, key in recvs:
                 b.recv[key] = engine.alloc_halo(engine.halo_count(d, key[1]))
             self.bufs[d] = (sends, recvs, b)
+        # peer-memory halo (one node): every rank maps the others' state slabs
+        # (CUDA IPC) and exchange_dir reads remote boundary layers directly
+        # over NVLink; a barrier per direction orders it.  PMHD_P2P_HALO=0
+        # keeps pack -> transport -> unpack.
+        self.p2p = False
+        import os
+        if (hasattr(engine, "peer_attach") and hasattr(transport, "allgather")
+                and os.environ.get("PMHD_P2P_HALO", "1") != "0"):
+            self.p2p = self._attach_peers(engine, plan, rank, transport)
         # stream-ordered stages: pack -> NCCL -> unpack all on the engine's
         # stream; the host synchronizes once per cycle (stage 2 status + dt)
         self.stream = None
@@ -185,7 +208,36 @@ class DistributedVL2:
             engine.set_async(True)
             self.stream = engine.torch_stream()
 
+    def _attach_peers(self, engine, plan, rank, transport):
+        base, handle = engine.slab()
+        handles = transport.allgather(handle)
+        self.peer_bases = []
+        ok = True
+        for r, h in enumerate(handles):
+            if r == rank:
+                self.peer_bases.append(None)
+                continue
+            try:
+                self.peer_bases.append(engine.ipc_open(h))
+            except Exception:  # no IPC / peer access: fall back for everyone
+                self.peer_bases.append(None)
+                ok = False
+        ok = all(transport.allgather(ok))
+        if not ok:
+            for b in self.peer_bases:
+                if b:
+                    engine.ipc_close(b)
+            self.peer_bases = []
+            return False
+        engine.peer_attach(plan.owners, self.peer_bases)
+        return True
+
     def exchange(self, half):
+        if self.p2p:  # direct peer reads: one barrier per sweep direction
+            for d in range(self.plan.dim):
+                self.tr.barrier(self.stream)
+                self.e.exchange_dir(d, half)
+            return
         for d in range(self.plan.dim):
             self.e.exchange_dir(d, half)
             sends, recvs, b = self.bufs[d]
@@ -225,9 +277,14 @@ class LoopbackWorld:
     orders send/recv on the issuing stream (DistributedVL2 over NCCL): the
     host never synchronizes inside a stage."""
 
-    def __init__(self, engines, plan, stream_ordered=False):
+    def __init__(self, engines, plan, stream_ordered=False, p2p=False):
         self.engines, self.plan = engines, plan
         self.stream_ordered = stream_ordered
+        self.p2p = p2p
+        if p2p:  # one process: the other engines' slabs are plain device pointers
+            bases = [e.slab()[0] for e in engines]
+            for r, e in enumerate(engines):
+                e.peer_attach(plan.owners, [None if q == r else b for q, b in enumerate(bases)])
         if stream_ordered:
             for e in engines:
                 e.set_async(True)
@@ -272,6 +329,11 @@ class LoopbackWorld:
                         self.streams[r].wait_event(copied[q])
 
     def exchange(self, half):
+        if self.p2p:  # direction-major: every engine's sweep d before any sweep d+1
+            for d in range(self.plan.dim):
+                for e in self.engines:
+                    e.exchange_dir(d, half)
+            return
         if self.stream_ordered:
             return self._exchange_streams(half)
         import torch

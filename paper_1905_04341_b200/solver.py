@@ -148,6 +148,28 @@ class GpuSolver:
         self._check(self.L.pmhd_gpu_stage_compute(self.mesh, s, dt, C.byref(dn), C.byref(st)), st)
         return dn.value, st
 
+    # ---- peer-memory halo (pmhd_gpu.h peer_attach) ---------------------------
+    def slab(self):
+        """(device base address, 64-byte CUDA IPC handle) of this mesh's state slab."""
+        base = C.c_void_p()
+        h = C.create_string_buffer(64)
+        self._check(self.L.pmhd_gpu_slab(self.mesh, C.byref(base), h))
+        return base.value, h.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        base = C.c_void_p()
+        self._check(self.L.pmhd_gpu_ipc_open(self.ctx, C.create_string_buffer(handle, 64), C.byref(base)))
+        return base.value
+
+    def ipc_close(self, base: int):
+        self._check(self.L.pmhd_gpu_ipc_close(self.ctx, C.c_void_p(base)))
+
+    def peer_attach(self, owners, bases):
+        """owners[gid] = rank; bases[rank] = that rank's slab as mapped here (None: unmapped)."""
+        own = (C.c_int * len(owners))(*owners)
+        arr = (C.c_void_p * len(bases))(*[C.c_void_p(b) if b else None for b in bases])
+        self._check(self.L.pmhd_gpu_peer_attach(self.mesh, len(bases), own, arr))
+
     def stage_prefetch(self, s, dt):
         """Stage s's interior flux tiles, overlapping the coming exchange."""
         self._check(self.L.pmhd_gpu_stage_prefetch(self.mesh, s, dt))

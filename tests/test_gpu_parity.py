@@ -263,23 +263,27 @@ MULTIRANK = {
 }
 
 
-@pytest.mark.parametrize("nranks,stream_ordered,case", [(2, False, "wave"), (4, False, "wave"),
-                                                        (2, True, "wave"), (4, True, "wave"),
-                                                        (2, True, "blast"), (4, True, "ot2d")])
-def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered, case):
+@pytest.mark.parametrize("nranks,stream_ordered,case,p2p", [(2, False, "wave", False), (4, False, "wave", False),
+                                                            (2, True, "wave", False), (4, True, "wave", False),
+                                                            (2, True, "blast", False), (4, True, "ot2d", False),
+                                                            (2, False, "wave", True), (4, False, "blast", True),
+                                                            (4, False, "ot2d", True)])
+def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered, case, p2p):
     """The multi-rank data path (stage_compute + local sweeps + halo pack /
     unpack kernels + transport) with nranks rank-engines on ONE GPU, stepped in
     lockstep by the host (no kernel waits on another), is bit-identical to the
     oracle: the GPU side of SURVEY.md §8e.  stream_ordered: the async ABI mode
     with the hand-over ordered by events between the engines' streams (what
-    DistributedVL2 does with NCCL), i.e. no host synchronization in a stage."""
+    DistributedVL2 does with NCCL), i.e. no host synchronization in a stage.
+    p2p: remote faces read straight from the other engines' memory by the
+    exchange kernels (pmhd_gpu_peer_attach), no pack / unpack."""
     from paper_1905_04341_b200.parallel import plan_for, LoopbackWorld
     cfg = RunConfig(**MULTIRANK[case])
     plan = plan_for(cfg, nranks)
     engines = [GpuSolver(cfg, parity=True, gids=plan.local_gids(r)) for r in range(nranks)]
     for e in engines:
         e.load_pgen(exchange=False)
-    world = LoopbackWorld(engines, plan, stream_ordered=stream_ordered)
+    world = LoopbackWorld(engines, plan, stream_ordered=stream_ordered, p2p=p2p)
     world.exchange(half=0)
     if stream_ordered:
         for s in world.streams:
@@ -409,3 +413,58 @@ def test_gpu_restart_bitwise_continuous(gpu_available, tmp_path):
         assert dt == dts[3 + q]
     for g in range(cfg.nblocks):
         assert np.array_equal(ref.get_block(g).u, b.get_block(g).u), g
+
+
+def _ipc_worker(rank, world, port, kw, ncyc, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1905_04341_b200.parallel import plan_for, DistributedVL2, TorchDistTransport
+        cfg = RunConfig(**kw)
+        plan = plan_for(cfg, world)
+        eng = GpuSolver(cfg, parity=True, gids=plan.local_gids(rank))
+        eng.load_pgen(exchange=False)
+        drv = DistributedVL2(eng, plan, rank, TorchDistTransport(dist, host_staging=True))
+        assert drv.p2p  # peer-memory halo over CUDA IPC
+        drv.exchange(half=0)
+        dt = drv.new_dt()
+        for _ in range(ncyc):
+            dt, _ = drv.vl2_step(dt)
+        q.put((rank, dt, {gid: eng.get_block(gid).u for gid in eng.gids}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ipc_peer_halo_two_processes(gpu_available):
+    """Two rank processes on one GPU, halo read over CUDA IPC peer memory
+    (host barriers between sweep directions, no kernel waits on another):
+    bit-identical to the oracle in one process."""
+    import socket
+    import torch.multiprocessing as mp
+    kw = MULTIRANK["blast"]
+    cfg = RunConfig(**kw)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, kw, 3, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    o = OracleSolver(cfg, workers=8)
+    o.load_pgen()
+    dt = o.new_dt()
+    for _ in range(3):
+        dt, _ = o.vl2_step(dt)
+    for rank, dtr, blocks in res:
+        assert dtr == dt
+        for gid, u in blocks.items():
+            assert np.array_equal(u, o.get_block(gid).u), (rank, gid)
