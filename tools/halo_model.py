@@ -1,9 +1,19 @@
 """Weak-scaling projection for the N>1 bench flow, from one-GPU measurements
-(no kernel waits on another): the halo bytes a rank sends per stage (exact,
-pmhd_gpu_halo_count), the measured pack / unpack kernel times of a 256^3
-rank-engine, and the measured stage time, against the NVLink peer-copy
-bandwidth the profiling recipe gives (770 GB/s per direction).  Prints a
-JSON line; it is a model, not a multi-GPU measurement.
+(no kernel waits on another).  A 2-rank (2n) x n x n line decomposition is
+built as two rank-engines on one GPU; measured with CUDA events in
+stream-ordered mode:
+
+* pack / transport / unpack path: the pack + unpack kernels of a stage's
+  halo (exact bytes from pmhd_gpu_halo_count) + the NVLink wire time at the
+  profiling recipe's measured peer-copy bandwidth (770 GB/s per direction);
+* peer-memory path (default on one node): the three exchange sweeps reading
+  the other engine's memory (here local HBM; on the box the remote part
+  crosses NVLink, added as wire time) + three barriers (~10 us each, an
+  NCCL one-int all-reduce).
+
+The stage-1 exchange overlaps the stage-2 interior flux tiles; the stage-2
+exchange and the 8-byte dt all-reduce are exposed.  Prints a JSON line: a
+model, not a multi-GPU measurement.
 
 usage: python tools/halo_model.py [n]      (n^3 cells per rank, default 256)
 """
@@ -21,20 +31,22 @@ from paper_1905_04341_b200.parallel import plan_for  # noqa: E402
 from paper_1905_04341_b200.solver import GpuSolver  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-NVLINK = 770e9  # measured peer copy per direction (B200_PROFILING.md)
-ranks = 2
-cfg = bench.make_config(n, ranks)  # (2n) x n x n, one block per rank
-plan = plan_for(cfg, ranks)
-g = GpuSolver(cfg, gids=plan.local_gids(0))
-g.load_pgen(exchange=False)
-g.set_async(True)  # stream-ordered calls (as over NCCL): the events time the kernels, not host syncs
+NVLINK = 770e9
+BARRIER_MS = 0.010
+cfg = bench.make_config(n, 2)
+plan = plan_for(cfg, 2)
+engs = [GpuSolver(cfg, gids=plan.local_gids(r)) for r in range(2)]
+for e in engs:
+    e.load_pgen(exchange=False)
+    e.set_async(True)
+g = engs[0]
 stream = torch.cuda.ExternalStream(g.stream_handle)
-sends, recvs = plan.messages(0, 0)
+sends, _ = plan.messages(0, 0)
 bufs = [(gid, side, g.alloc_halo(g.halo_count(0, 1 - side))) for _, _, gid, side in sends]
 msg_bytes = sum(b.numel() * 8 for _, _, b in bufs)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 dt = g.new_dt()
-for _ in range(2):  # warm-up
+for _ in range(2):
     g.stage_compute(1, dt)
 reps = 5
 ev[0].record(stream)
@@ -47,16 +59,26 @@ for _ in range(reps):
     for gid, side, b in bufs:
         g.halo_unpack(gid, 0, side, 1, b)
 ev[2].record(stream)
+# peer-memory sweeps: engine 0 reads engine 1's slab directly
+bases = [e.slab()[0] for e in engs]
+g.peer_attach(plan.owners, [None, bases[1]])
+for _ in range(reps):
+    for d in range(cfg.dim):
+        g.exchange_dir(d, 1)
+ev[3].record(stream)
 torch.cuda.synchronize()
 stage_ms = ev[0].elapsed_time(ev[1]) / reps
 packunpack_ms = ev[1].elapsed_time(ev[2]) / reps
+sweeps_ms = ev[2].elapsed_time(ev[3]) / reps
 wire_ms = msg_bytes / NVLINK * 1e3
-# per stage: the stage-1 exchange overlaps the stage-2 interior tiles (~75 % of
-# the flux work), the stage-2 one is exposed; + ~20 us for the dt all-reduce
-exposed_ms = 0.5 * (packunpack_ms + wire_ms) + 0.01
-eff = stage_ms / (stage_ms + exposed_ms)
-print(json.dumps({"cells_per_rank": n ** 3, "halo_bytes_per_stage": msg_bytes,
-                  "stage_ms": stage_ms, "pack_unpack_ms": packunpack_ms,
-                  "nvlink_wire_ms_at_770GBps": wire_ms,
-                  "projected_weak_efficiency": eff,
-                  "note": "model from one-GPU measurements; not a multi-GPU run"}))
+# both paths run the three sweeps (local faces; the p2p sweeps also read the
+# remote ones); the pack path adds the pack / unpack kernels
+x_pack = sweeps_ms + packunpack_ms + wire_ms
+x_p2p = sweeps_ms + wire_ms + 3 * BARRIER_MS
+res = {"cells_per_rank": n ** 3, "halo_bytes_per_stage": msg_bytes, "stage_ms": stage_ms,
+       "pack_unpack_ms": packunpack_ms, "p2p_sweeps_ms": sweeps_ms,
+       "nvlink_wire_ms_at_770GBps": wire_ms,
+       "projected_weak_efficiency_pack": stage_ms / (stage_ms + 0.5 * x_pack + 0.01),
+       "projected_weak_efficiency_p2p": stage_ms / (stage_ms + 0.5 * x_p2p + 0.01),
+       "note": "model from one-GPU measurements (tools/halo_model.py); not a multi-GPU run"}
+print(json.dumps(res))
