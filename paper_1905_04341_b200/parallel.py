@@ -25,6 +25,7 @@ alloc_halo / halo_pack / halo_unpack / gids.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 
@@ -195,14 +196,12 @@ class DistributedVL2:
         # over NVLink; a barrier per direction orders it.  PMHD_P2P_HALO=0
         # keeps pack -> transport -> unpack.
         self.p2p = False
-        import os
         if (hasattr(engine, "peer_attach") and hasattr(transport, "allgather")
                 and os.environ.get("PMHD_P2P_HALO", "1") != "0"):
             self.p2p = self._attach_peers(engine, plan, rank, transport)
-        # stream-ordered stages: pack -> NCCL -> unpack all on the engine's
-        # stream; the host synchronizes once per cycle (stage 2 status + dt)
+        # stream-ordered stages: halo sweeps / NCCL on the engine's stream;
+        # the host synchronizes once per cycle (stage 2 status + dt)
         self.stream = None
-        import os
         if (getattr(transport, "stream_ordered", False) and hasattr(engine, "set_async")
                 and os.environ.get("PMHD_SYNC_HALO", "0") != "1"):
             engine.set_async(True)
