@@ -13,10 +13,14 @@ for both:
   boundary; then an all-reduce(min) of dt.  With the sweeps kept sequential,
   the result is bit-identical to the single-process exchange.
 
-Transports: ``TorchDistTransport`` (torch.distributed P2P; NCCL over NVLink
-for CUDA buffers, gloo for CPU buffers) and ``LoopbackTransport`` (several
-engines in one process, used to test the GPU pack/unpack path on one GPU
-without kernels that wait on each other).
+Halo data paths: the peer-memory halo (default for GPU engines on one node:
+the ranks map each other's state slabs over CUDA IPC and the exchange kernels
+read remote boundary layers directly over NVLink, one barrier per sweep
+direction), or pack -> transport -> unpack.  Transports:
+``TorchDistTransport`` (torch.distributed: NCCL over NVLink, ordered on the
+engine's stream; gloo for CPU buffers) and ``LoopbackWorld`` (several engines
+in one process, used to test every GPU path on one GPU without kernels that
+wait on each other).
 
 An *engine* is ``solver.GpuSolver`` (product) or, in tests only, the CPU
 oracle binding; both expose stage_compute / exchange_dir / halo_count /
