@@ -907,7 +907,8 @@ class Mesh {
   //--------------------------------------------------------------------------
   // Turbulence driving (definition in include/pmhd_host.h,
   // GPU: kernels_drive.cu).  dv per local block on active cells; sums per
-  // block with each (k, j) row summed over i and rows in (k, j) order.
+  // block: each (k, j) row summed over i, each k plane over its rows in j
+  // order, the block over its planes in k order.
   std::vector<Field<R>> dvel;  // 3 per local block
 
   void drive_begin(int nmode, const int* kv, const double* cv, const double* sv,
@@ -918,7 +919,8 @@ class Mesh {
       Field<R>* D = &dvel[3 * b];
       for (int a = 0; a < 3; ++a) D[a].resize(g.n[2], g.n[1], g.n[0]);
       R s0 = R(0.0), s1 = R(0.0), s2 = R(0.0), s3 = R(0.0);
-      for (int k = g.ks; k < g.ke; ++k)
+      for (int k = g.ks; k < g.ke; ++k) {
+        R p0 = R(0.0), p1 = R(0.0), p2 = R(0.0), p3 = R(0.0);  // plane sums (rows in j order)
         for (int j = g.js; j < g.je; ++j) {
           R r0 = R(0.0), r1 = R(0.0), r2 = R(0.0), r3 = R(0.0);
           for (int i = g.is; i < g.ie; ++i) {
@@ -946,8 +948,10 @@ class Mesh {
             r2 = r2 + rho * dv1;
             r3 = r3 + rho * dv2;
           }
-          s0 = s0 + r0; s1 = s1 + r1; s2 = s2 + r2; s3 = s3 + r3;
+          p0 = p0 + r0; p1 = p1 + r1; p2 = p2 + r2; p3 = p3 + r3;
         }
+        s0 = s0 + p0; s1 = s1 + p1; s2 = s2 + p2; s3 = s3 + p3;
+      }
       sums[4 * b] = value_of(s0); sums[4 * b + 1] = value_of(s1); sums[4 * b + 2] = value_of(s2); sums[4 * b + 3] = value_of(s3);
     }
   }
@@ -957,7 +961,8 @@ class Mesh {
       Block<R>& B = blocks[b];
       const Field<R>* D = &dvel[3 * b];
       R s0 = R(0.0), s1 = R(0.0);
-      for (int k = g.ks; k < g.ke; ++k)
+      for (int k = g.ks; k < g.ke; ++k) {
+        R p0 = R(0.0), p1 = R(0.0);
         for (int j = g.js; j < g.je; ++j) {
           R r0 = R(0.0), r1 = R(0.0);
           for (int i = g.is; i < g.ie; ++i) {
@@ -967,8 +972,10 @@ class Mesh {
             r0 = r0 + 0.5 * rho * q;
             r1 = r1 + (B.A.u[IM1](k, j, i) * p0 + B.A.u[IM2](k, j, i) * p1 + B.A.u[IM3](k, j, i) * p2);
           }
-          s0 = s0 + r0; s1 = s1 + r1;
+          p0 = p0 + r0; p1 = p1 + r1;
         }
+        s0 = s0 + p0; s1 = s1 + p1;
+      }
       sums[4 * b] = value_of(s0); sums[4 * b + 1] = value_of(s1); sums[4 * b + 2] = 0.0; sums[4 * b + 3] = 0.0;
     }
   }

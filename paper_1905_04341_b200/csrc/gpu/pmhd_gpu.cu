@@ -75,7 +75,7 @@ struct pmhd_mesh {
   bool overlap = false;           // on for meshes with remote neighbours; PMHD_OVERLAP=0/1 overrides
   // turbulence driving buffers (allocated at the first event)
   double* drive_tab = nullptr;    // 3 axes x (cos, sin) x 5 x nx[a]
-  double* drive_rows = nullptr;   // nb x rows x 4
+  double* drive_rows = nullptr;   // nb x rows x 4, then nb x planes x 4
   double* drive_sums = nullptr;   // nb x 4
   DriveTabs drive{};
   int variant = 0;                // 0: fused flux kernels; 1: split (debug; PMHD_KERNELS=split)
@@ -978,7 +978,7 @@ int pmhd_gpu_drive_begin(pmhd_mesh* m, int nmode, const int* k, const double* c,
   const KGeom& G = m->G;
   if (!m->drive_tab) {
     const size_t tab = 2 * 5 * size_t(G.nx[0] + G.nx[1] + G.nx[2]);
-    const size_t rows = size_t(G.nb) * (G.ke - G.ks) * (G.je - G.js) * 4;
+    const size_t rows = size_t(G.nb) * (G.ke - G.ks) * ((G.je - G.js) + 1) * 4;  // rows + planes
     CK(cudaMalloc(&m->drive_tab, tab * sizeof(double)));
     CK(cudaMalloc(&m->drive_rows, rows * sizeof(double)));
     CK(cudaMalloc(&m->drive_sums, size_t(G.nb) * 4 * sizeof(double)));
@@ -1004,7 +1004,7 @@ int pmhd_gpu_drive_begin(pmhd_mesh* m, int nmode, const int* k, const double* c,
   launch_drive_dv(m->dblk, G, T, ctx->stream);
   const double zero[3] = {0.0, 0.0, 0.0};
   launch_drive_sums(m->dblk, G, 0, zero, m->drive_rows, m->drive_sums, ctx->stream);
-  m->times.kernel_launches += 3;
+  m->times.kernel_launches += 4;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(sums, m->drive_sums, size_t(G.nb) * 4 * sizeof(double), cudaMemcpyDeviceToHost,
                      ctx->stream));
@@ -1016,7 +1016,7 @@ int pmhd_gpu_drive_energy(pmhd_mesh* m, const double* mean, double* sums) {
   if (!m || !mean || !sums || !m->drive_tab) return PMHD_ERR_INPUT;
   pmhd_ctx* ctx = m->ctx;
   launch_drive_sums(m->dblk, m->G, 1, mean, m->drive_rows, m->drive_sums, ctx->stream);
-  m->times.kernel_launches += 2;
+  m->times.kernel_launches += 3;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(sums, m->drive_sums, size_t(m->G.nb) * 4 * sizeof(double), cudaMemcpyDeviceToHost,
                      ctx->stream));

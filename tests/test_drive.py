@@ -49,7 +49,8 @@ def test_kick_injects_energy_without_momentum():
     E1, M1, K1 = totals(o, cfg)
     assert abs((E1 - E0) - de) <= 1e-11 * de  # all of it kinetic, exactly de
     assert abs((K1 - K0) - de) <= 1e-11 * de
-    assert np.abs(M1 - M0).max() <= 1e-13 * max(1.0, np.abs(M0).max())
+    # zero mean momentum up to summation rounding: ~ n_cells * eps * |m|
+    assert np.abs(M1 - M0).max() <= 16**3 * 2.2e-16 * max(1.0, np.abs(M0).max())
     # ghosts were refreshed: another exchange changes nothing
     before = [o.get_block(g).u.copy() for g in range(cfg.nblocks)]
     o.exchange()
