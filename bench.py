@@ -371,7 +371,8 @@ def run_ours(args):
         for a in arrs + outs:
             cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
         h2d = host.u[:5].nbytes + host.b1f.nbytes + host.b2f.nbytes + host.b3f.nbytes
-        d2h = out.u[:5].nbytes + out.b1f.nbytes + out.b2f.nbytes + out.b3f.nbytes
+        # the download returns all 8 cell variables (Bcc re-derived on the device) + faces
+        d2h = out.u.nbytes + out.b1f.nbytes + out.b2f.nbytes + out.b3f.nbytes
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
