@@ -37,6 +37,10 @@ namespace {
 #define PMHD_FLUX_X1_FX 32  // x1 tiles: faces along i
 #endif
 constexpr int NTHR = 128;
+#ifndef PMHD_FLUX_FACE_UNROLL
+#define PMHD_FLUX_FACE_UNROLL 1  // 2: both faces of a thread in one unrolled body
+#endif
+constexpr int kFaceUnroll = PMHD_FLUX_FACE_UNROLL;
 #ifndef PMHD_FLUX_SMEMW
 #define PMHD_FLUX_SMEMW 1
 #endif
@@ -228,7 +232,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   const int fc = threadIdx.x % FX;
   const double c1024 = (MODE == 2) ? kd->c1024[DIR] : c1024_arg;
   const double* const wsrc = plm ? &sp[0][0] : &sw[0][0];  // low-side cell's high-face value
-#pragma unroll 1
+#pragma unroll kFaceUnroll
   for (int h = 0; h < 2; ++h) {
     const int fr = threadIdx.x / FX + (NTHR / FX) * h;
     const int fi = fi0 + fc, fs = fs0 + fr;
