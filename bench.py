@@ -114,21 +114,32 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
                  "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
-            time.sleep(0.3)
+            # nvidia-smi can take a second to start on a fresh box: the timed
+            # region begins only once it is producing samples
+            t_end = time.perf_counter() + 15.0
+            while not self.lines and time.perf_counter() < t_end and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
+        self.t0 = time.perf_counter()
         return self
 
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.perf_counter(), ln.strip()))
 
     def __exit__(self, *a):
+        self.t1 = time.perf_counter()
         if self.proc:
+            # one sample past the end of the region (the last one taken under load)
+            t_end = self.t1 + 1.0
+            while (not self.lines or self.lines[-1][0] <= self.t1) and time.perf_counter() < t_end \
+                    and self.proc.poll() is None:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -138,7 +149,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # samples taken inside the timed region, plus the first one after it
+        inside = [ln for t, ln in self.lines if self.t0 <= t <= self.t1]
+        after = [ln for t, ln in self.lines if t > self.t1][:1]
+        for ln in inside + after:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -280,6 +294,7 @@ def run_ours(args):
         return drv.vl2_step(d)[0]
 
     dt = allreduce_min(dt)
+    clk = ClockSampler(local).__enter__()  # started before the warm-up: no idle gap before the region
     for _ in range(args.warmup):
         dt = step(dt)
     # ---- timed region (inputs resident in HBM, 1.5 GB state >> 126 MB L2) ----
@@ -287,12 +302,13 @@ def run_ours(args):
     g.region_times(reset=True)
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        evs[0].record(stream)
-        for k in range(args.steps):
-            dt = step(dt)
-            evs[k + 1].record(stream)
-        torch.cuda.synchronize()
+    clk.t0 = time.perf_counter()
+    evs[0].record(stream)
+    for k in range(args.steps):
+        dt = step(dt)
+        evs[k + 1].record(stream)
+    torch.cuda.synchronize()
+    clk.__exit__(None, None, None)
     barrier()
     launches = g.region_times()["kernel_launches"]
     per_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
