@@ -131,7 +131,7 @@ void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStrea
 // ring with TMA, one plane ahead.  Box extents: update_ec_box().
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                          const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s,
-                         const CUtensorMap* ec_maps = nullptr);
+                         const CUtensorMap* ec_maps = nullptr, int push = 0);
 void update_ec_box(int box[2]);
 bool update_uses_tma();  // built with PMHD_UPDATE_TMA
 void launch_update(const DevBlock* blks, const KGeom& G, const KStage& ks, cudaStream_t s);

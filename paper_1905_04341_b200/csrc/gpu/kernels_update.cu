@@ -104,7 +104,7 @@ template <int SEG, int MODE>
 __global__ void __launch_bounds__(UTHR, PMHD_UPDATE_MINB)
 k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_arg,
                const KStage* __restrict__ kd, DevRed* red, int want_dt, int kr0, int kr1,
-               const CUtensorMap* __restrict__ ec_maps) {
+               const CUtensorMap* __restrict__ ec_maps, int push) {
   // graph-replayed cycle past the end of the run: tested after the prologue's
   // E loads are issued (before any global write)
   constexpr bool PROF = (MODE == 1);
@@ -146,6 +146,19 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
   const int tid = threadIdx.x;
   const int mode = ph.emf;
   const double c1 = ks.c1, c2 = ks.c2, c3 = ks.c3;
+  // x1 ghost push (all x1 neighbours local, launch flag): every value this
+  // kernel writes that the x1 ghost exchange would copy is also stored at
+  // its ghost position in the neighbour block, so the stage's x1 exchange
+  // launch is skipped.  PL: the left neighbour (its right ghosts come from
+  // cells [is, is+ng)), PR: the right neighbour (left ghosts from
+  // [ie-ng, ie)); for b1f the normal-face ranges of the exchange apply, and
+  // the shared face is is left to the left neighbour's ie face.
+  double* const* PL = push ? blks[B.nbr[0][0]].st[ks.out_sel] : nullptr;
+  double* const* PR = push ? blks[B.nbr[0][1]].st[ks.out_sel] : nullptr;
+  auto push_cell = [&](int v, int i, int id, double val) {
+    if (i < G.is + G.ng) ST(PL[v] + id + G.mb[0], val);
+    if (i >= G.ie - G.ng) ST(PR[v] + id - G.mb[0], val);
+  };
 
   // cell-centred E of plane kk (written by the last-direction flux kernel
   // from the stage-input primitives) into ring slot kk & 1
@@ -289,7 +302,14 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       if (d3) v = Sb[5][id] - (c2 * (e3s[r + 1][c] - e3s[r][c]) - c3 * (e2s[hi][r][c] - e2s[lo][r][c]));
       else v = Sb[5][id] - c2 * (e3s[r + 1][c] - e3s[r][c]);
       b1s[r][c] = v;
-      if (c < nx || i0 + c == G.ie) ST(Sout[5] + id, v);
+      if (c < nx || i0 + c == G.ie) {
+        const int i = i0 + c;
+        if (!push || i != G.is) ST(Sout[5] + id, v);
+        if (push) {
+          if (i > G.is && i <= G.is + G.ng) ST(PL[5] + id + G.mb[0], v);
+          if (i >= G.ie - G.ng) ST(PR[5] + id - G.mb[0], v);
+        }
+      }
     }
     for (int q = tid; q < (UY + 1) * UX; q += UTHR) {  // b2f, faces j0 .. j0+ny
       const int c = q % UX, r = q / UX;
@@ -299,7 +319,10 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       if (d3) v = Sb[6][id] - (c3 * (e1s[hi][r][c] - e1s[lo][r][c]) - c1 * (e3s[r][c + 1] - e3s[r][c]));
       else v = Sb[6][id] + c1 * (e3s[r][c + 1] - e3s[r][c]);
       b2s[r][c] = v;
-      if (r < ny || j0 + r == G.je) ST(Sout[6] + id, v);
+      if (r < ny || j0 + r == G.je) {
+        ST(Sout[6] + id, v);
+        if (push) push_cell(6, i0 + c, id, v);
+      }
     }
     face_b3(k + 1, hi);  // b3 at face k + 1 (face k carried)
     {
@@ -308,6 +331,10 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
         const int id = G.idx(k, j0 + r, i0 + c);
         ST(Sout[7] + id, b3s[lo][r][c]);
         if (k + 1 == G.ke) ST(Sout[7] + id + sy, b3s[hi][r][c]);
+        if (push) {
+          push_cell(7, i0 + c, id, b3s[lo][r][c]);
+          if (k + 1 == G.ke) push_cell(7, i0 + c, id + sy, b3s[hi][r][c]);
+        }
       }
     }
     __syncthreads();
@@ -341,6 +368,10 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
         }
 #pragma unroll
         for (int v = 0; v < 5; ++v) ST(Sout[v] + id, u[v]);
+        if (push) {
+#pragma unroll
+          for (int v = 0; v < 5; ++v) push_cell(v, i, id, u[v]);
+        }
         if (want_dt) {
           const double d = w[0], p = w[4];
           const double cf1 = fast_speed_n(d, p, w[5], w[6], w[7], ph.gamma);
@@ -386,7 +417,7 @@ bool update_uses_tma() { return PMHD_UPDATE_TMA != 0; }
 
 void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                          const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s,
-                         const CUtensorMap* ec_maps) {
+                         const CUtensorMap* ec_maps, int push) {
   // segment length: PMHD_UPDATE_SEG planes, or 4 / 1 when the mesh is too
   // small to fill ~2 waves of 148 SMs x 5 CTAs otherwise
   const int tiles = ((G.ie - G.is + UX - 1) / UX) * ((G.je - G.js + UY - 1) / UY) * G.nb;
@@ -409,11 +440,11 @@ void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, 
       attr_devs |= 1ULL << (dev & 63);                                                                  \
     }                                                                                                   \
     if (kd)                                                                                             \
-      k_update_fused<SG, 2><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps);      \
+      k_update_fused<SG, 2><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps, push);      \
     else if (ph.prof)                                                                                   \
-      k_update_fused<SG, 1><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps);      \
+      k_update_fused<SG, 1><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps, push);      \
     else                                                                                                \
-      k_update_fused<SG, 0><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps);      \
+      k_update_fused<SG, 0><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps, push);      \
   } while (0)
   if (seg == PMHD_UPDATE_SEG) PMHD_UPDATE_LAUNCH(PMHD_UPDATE_SEG);
   else if (seg == 4) PMHD_UPDATE_LAUNCH(4);

@@ -80,6 +80,7 @@ struct pmhd_mesh {
   DriveTabs drive{};
   int variant = 0;                // 0: fused flux kernels; 1: split (debug; PMHD_KERNELS=split)
   int slab_planes = 0;            // k-slab pipeline depth (PMHD_SLAB_PLANES, 0 = off)
+  bool push_x1 = false;           // update kernel writes the x1 ghosts (PMHD_PUSH_X1, default on when possible)
   std::vector<cudaEvent_t> slab_ev;
   cudaEvent_t ev[8] = {};
   pmhd_region_times times{};
@@ -298,7 +299,8 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     if (m->variant == 1) launch_emf(m->dblk, G, m->ph, st);
     rec(m, 3);
     if (m->variant == 0) {
-      launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks, G.ke, st, m->ec_maps);
+      launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks, G.ke, st, m->ec_maps,
+                          m->push_x1 ? 1 : 0);
     } else {
       launch_update(m->dblk, G, ks, st);
       launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
@@ -308,9 +310,12 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
       int rc = prefetch_stage(m, 2, dt);
       if (rc) return rc;
     }
-    if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st, kd);
+    // (x1 ghosts already stored by the update kernel when pushed)
+    const int d0 = (m->variant == 0 && m->push_x1) ? 1 : 0;
+    if (do_exchange)
+      for (int dir = d0; dir < G.dim; ++dir) launch_exchange_dir(m->dblk, G, ks.out_sel, dir, st, kd);
     rec(m, 5);
-    m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim : 4 + G.dim) + (do_exchange ? G.dim : 0);
+    m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim : 4 + G.dim) + (do_exchange ? G.dim - d0 : 0);
   }
   CK(cudaGetLastError());
   if (s == 2) {  // u^{n+1} (st[2]) becomes the current state: flip the tables
@@ -570,6 +575,16 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   // stage and splitting the flux launches costs more (measured -1.4 % at 256^3).
   m->overlap = !m->all_local;
   if (const char* ov = std::getenv("PMHD_OVERLAP")) m->overlap = std::atoi(ov) != 0;
+  // x1 ghost push: every block's x1 neighbours local and mutual (regular
+  // periodic decomposition), so the update kernel can store the x1 ghost
+  // layers itself and the in-stage x1 exchange launch is dropped
+  m->push_x1 = true;
+  for (int b = 0; b < G.nb; ++b) {
+    const int L = m->hblk[b].nbr[0][0], R = m->hblk[b].nbr[0][1];
+    if (L < 0 || R < 0 || m->hblk[L].nbr[0][1] != b || m->hblk[R].nbr[0][0] != b) m->push_x1 = false;
+  }
+  if (G.mb[0] < G.ng) m->push_x1 = false;
+  if (const char* px = std::getenv("PMHD_PUSH_X1")) m->push_x1 = m->push_x1 && std::atoi(px) != 0;
   m->slab_ev.resize((G.ke - G.ks) / 8 + 2);
   for (auto& e : m->slab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -799,7 +814,7 @@ int graph_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int
   // cycles that ran: the completed ones, plus the failing one (its stages ran
   // and flipped the tables inside the graph)
   const int ran = c.cycles + (c.err_key != ULLONG_MAX ? 1 : 0);
-  const long long per_cycle = 2 + 2 * (2 * G.dim + 1);
+  const long long per_cycle = 2 + 2 * (2 * G.dim + 1 - (m->push_x1 ? 1 : 0));
   m->times.kernel_launches += per_cycle * ran;
   if (ran & 1) {  // the state is in the other table after an odd number of cycles
     std::swap(m->hblk, m->hblk_alt);

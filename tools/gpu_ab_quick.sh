@@ -6,6 +6,7 @@ B="python bench.py --steps 6 --warmup 3 --no-cpu-baseline --no-e2e"
 for rep in 1 2; do
 for v in "$@"; do
   if [ "$v" = default ]; then $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err
+  elif [[ "$v" == *=* ]]; then env "$v" $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err
   else PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_$v.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err; fi
   python - "$v" <<'PY'
 import json,sys
