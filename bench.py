@@ -58,11 +58,28 @@ def dist_env():
     return ws, rank, local
 
 
+def rank_grid(ranks):
+    """Rank grid (p1, p2, p3) of the M4 weak-scaling run:
+    (1,1,1), (2,1,1), (2,2,1), (2,2,2) for 1 / 2 / 4 / 8 ranks -- each prime
+    factor of the rank count goes to the axis with the fewest ranks so far."""
+    from paper_1905_04341_b200.parallel import _factor
+    p = [1, 1, 1]
+    for f in sorted(_factor(ranks), reverse=True):
+        a = min(range(3), key=lambda x: p[x])
+        p[a] *= f
+    return p
+
+
 def make_config(n, ranks, riemann="hlld", nz=None):
+    """The M4 linear fast wave: one n^3 MeshBlock per rank on a (p1 n) x
+    (p2 n) x (p3 n) periodic grid with dx = 1/n (nz: the CPU legs' bounded
+    n x n x nz slab, one rank)."""
     from paper_1905_04341_b200 import RunConfig
+    p = rank_grid(ranks)
     nz = n if nz is None else nz
-    return RunConfig(nx1=n * ranks, nx2=n, nx3=nz, mb1=n, mb2=n, mb3=nz, x1max=float(ranks),
-                     x3max=nz / n, wave_mode=6, wave_amp=1e-6, cfl=0.3, riemann=riemann)
+    return RunConfig(nx1=n * p[0], nx2=n * p[1], nx3=nz * p[2], mb1=n, mb2=n, mb3=nz, x1max=float(p[0]),
+                     x2max=float(p[1]), x3max=p[2] * nz / n, wave_mode=6, wave_amp=1e-6, cfl=0.3,
+                     riemann=riemann)
 
 
 def falg():
@@ -429,7 +446,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (linear-wave problem generator)",
             "config": {"workload": f"M4 3D linear fast wave, {n}^3 active cells per GPU in one MeshBlock, "
                                    f"HLLD+PLM(MC)+CT, CFL 0.3, A=1e-6",
-                       "global_cells": [n * ws, n, n], "parallelism": f"{ws} rank(s), one {n}^3 block each",
+                       "global_cells": [n * q for q in rank_grid(ws)],
+                       "parallelism": (f"{ws} rank(s) as a {'x'.join(map(str, rank_grid(ws)))} grid of {n}^3 "
+                                       f"blocks, one per rank"),
                        "l2": (f"inputs larger than L2 ({8 * 8 * (n + 4) ** 3 / 1e9:.2f} GB state per GPU "
                               f"vs 126 MB L2)" if 64 * (n + 4) ** 3 > 126e6 else
                               "state smaller than L2 (small validation size)"),

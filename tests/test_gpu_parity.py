@@ -267,7 +267,8 @@ MULTIRANK = {
                                                             (2, True, "wave", False), (4, True, "wave", False),
                                                             (2, True, "blast", False), (4, True, "ot2d", False),
                                                             (2, False, "wave", True), (4, False, "blast", True),
-                                                            (4, False, "ot2d", True)])
+                                                            (4, False, "ot2d", True), (8, False, "blast", True),
+                                                            (8, True, "blast", False)])
 def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered, case, p2p):
     """The multi-rank data path (stage_compute + local sweeps + halo pack /
     unpack kernels + transport) with nranks rank-engines on ONE GPU, stepped in

@@ -14,6 +14,8 @@ from paper_1905_04341_b200.parallel import partition, plan_for, HaloPlan
 CFG = dict(nx1=32, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, x2max=0.5, x3max=0.5, wave_n1=1,
            wave_n2=1, wave_amp=1e-3)
 CFG2D = dict(nx1=64, nx2=64, nx3=1, mb1=16, mb2=32, mb3=1, pgen="orszag_tang", cfl=0.4)
+# 2 x 2 x 2 blocks on 8 ranks: every neighbour remote, the same rank on both sides
+CFG8 = dict(nx1=16, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, wave_n1=1, wave_n2=1, wave_amp=1e-3)
 CFGTURB = dict(nx1=16, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, pgen="turbulence", turb_drive=1,
                turb_dedt=0.5, turb_every=2)
 
@@ -84,7 +86,7 @@ def _worker(rank, world, port, cfg_kw, ncyc, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,cfg_kw", [(2, CFG), (4, CFG), (2, CFG2D), (2, CFGTURB)])
+@pytest.mark.parametrize("world,cfg_kw", [(2, CFG), (4, CFG), (2, CFG2D), (2, CFGTURB), (8, CFG8)])
 def test_gloo_sharded_equals_single_process(world, cfg_kw):
     import torch.multiprocessing as mp
     from oracle.binding import OracleSolver
