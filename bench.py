@@ -44,6 +44,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--size", type=int, default=256, help="cells per dimension per GPU")
+    p.add_argument("--block", type=int, default=0,
+                   help="MeshBlock edge (default = --size: one block per GPU; 128 with --size 256: the "
+                        "8-blocks-per-GPU M4 variant)")
     p.add_argument("--riemann", default="hlld")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -70,14 +73,15 @@ def rank_grid(ranks):
     return p
 
 
-def make_config(n, ranks, riemann="hlld", nz=None):
-    """The M4 linear fast wave: one n^3 MeshBlock per rank on a (p1 n) x
-    (p2 n) x (p3 n) periodic grid with dx = 1/n (nz: the CPU legs' bounded
-    n x n x nz slab, one rank)."""
+def make_config(n, ranks, riemann="hlld", nz=None, block=0):
+    """The M4 linear fast wave: n^3 cells per rank on a (p1 n) x (p2 n) x
+    (p3 n) periodic grid with dx = 1/n, in MeshBlocks of block^3 (default:
+    one n^3 block per rank; nz: the CPU legs' bounded n x n x nz slab)."""
     from paper_1905_04341_b200 import RunConfig
     p = rank_grid(ranks)
     nz = n if nz is None else nz
-    return RunConfig(nx1=n * p[0], nx2=n * p[1], nx3=nz * p[2], mb1=n, mb2=n, mb3=nz, x1max=float(p[0]),
+    mb = block if block else n
+    return RunConfig(nx1=n * p[0], nx2=n * p[1], nx3=nz * p[2], mb1=mb, mb2=mb, mb3=min(mb, nz), x1max=float(p[0]),
                      x2max=float(p[1]), x3max=p[2] * nz / n, wave_mode=6, wave_amp=1e-6, cfl=0.3,
                      riemann=riemann)
 
@@ -275,16 +279,18 @@ def run_ours(args):
     from paper_1905_04341_b200 import native as N
 
     n = args.size
-    # global (n*ws) x n x n periodic mesh, one n^3 MeshBlock per rank
-    cfg = make_config(n, ws, riemann=args.riemann)
+    # (p1 n) x (p2 n) x (p3 n) periodic mesh, n^3 cells per rank (one block,
+    # or --block edge blocks)
+    cfg = make_config(n, ws, riemann=args.riemann, block=args.block)
     cells_rank = n ** 3
     from paper_1905_04341_b200.parallel import plan_for, DistributedVL2, TorchDistTransport
     plan = plan_for(cfg, ws)
-    my_gid = plan.local_gids(rank)[0]
-    g = GpuSolver(cfg, device=local, gids=[my_gid])
+    my_gids = plan.local_gids(rank)
+    g = GpuSolver(cfg, device=local, gids=my_gids)
     stream = torch.cuda.ExternalStream(g.stream_handle, device=torch.device("cuda", local))
-    host = cfg.pgen_block(my_gid)
-    g.set_block(my_gid, host)
+    hosts = {gid: cfg.pgen_block(gid) for gid in my_gids}
+    for gid, hb in hosts.items():
+        g.set_block(gid, hb)
     drv = None
     if dist is not None:
         drv = DistributedVL2(g, plan, rank, TorchDistTransport(dist, host_staging=GLOO_HOST),
@@ -398,19 +404,20 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         cudart = torch.cuda.cudart()
-        arrs = [host.u, host.b1f, host.b2f, host.b3f]
-        out = cfg.new_block()
-        outs = [out.u, out.b1f, out.b2f, out.b3f]
+        outb = {gid: cfg.new_block() for gid in my_gids}
+        arrs = [a for hb in hosts.values() for a in (hb.u, hb.b1f, hb.b2f, hb.b3f)]
+        outs = [a for ob in outb.values() for a in (ob.u, ob.b1f, ob.b2f, ob.b3f)]
         for a in arrs + outs:
             cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
-        h2d = host.u[:5].nbytes + host.b1f.nbytes + host.b2f.nbytes + host.b3f.nbytes
+        h2d = sum(hb.u[:5].nbytes + hb.b1f.nbytes + hb.b2f.nbytes + hb.b3f.nbytes for hb in hosts.values())
         # the download returns all 8 cell variables (Bcc re-derived on the device) + faces
-        d2h = out.u.nbytes + out.b1f.nbytes + out.b2f.nbytes + out.b3f.nbytes
+        d2h = sum(a.nbytes for a in outs)
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        g.set_block(my_gid, host)
+        for gid, hb in hosts.items():
+            g.set_block(gid, hb)
         if drv is None:
             g.exchange()
         else:
@@ -418,7 +425,8 @@ def run_ours(args):
         d = allreduce_min(g.new_dt())
         for _ in range(args.steps):
             d = step(d)
-        g.get_block(my_gid, out=out)
+        for gid, ob in outb.items():
+            g.get_block(gid, out=ob)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
@@ -444,11 +452,12 @@ def run_ours(args):
             "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (linear-wave problem generator)",
-            "config": {"workload": f"M4 3D linear fast wave, {n}^3 active cells per GPU in one MeshBlock, "
-                                   f"HLLD+PLM(MC)+CT, CFL 0.3, A=1e-6",
+            "config": {"workload": (f"M4 3D linear fast wave, {n}^3 active cells per GPU in "
+                                    f"{len(my_gids)} MeshBlock(s) of {cfg.desc.mb[0]}^3, "
+                                    f"HLLD+PLM(MC)+CT, CFL 0.3, A=1e-6"),
                        "global_cells": [n * q for q in rank_grid(ws)],
                        "parallelism": (f"{ws} rank(s) as a {'x'.join(map(str, rank_grid(ws)))} grid of {n}^3 "
-                                       f"blocks, one per rank"),
+                                       f"bricks, one per rank"),
                        "l2": (f"inputs larger than L2 ({8 * 8 * (n + 4) ** 3 / 1e9:.2f} GB state per GPU "
                               f"vs 126 MB L2)" if 64 * (n + 4) ** 3 > 126e6 else
                               "state smaller than L2 (small validation size)"),
