@@ -96,6 +96,17 @@ namespace {
       return PMHD_ERR_CUDA;                                                    \
     }                                                                          \
   } while (0)
+// CK inside pmhd_gpu_mesh_create once the mesh exists: free what was
+// allocated so far (every handle starts null) before returning
+#define MCK(call)                                                              \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);          \
+      pmhd_gpu_mesh_destroy(m);                                                \
+      return PMHD_ERR_CUDA;                                                    \
+    }                                                                          \
+  } while (0)
 
 int fail(pmhd_ctx* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
@@ -551,25 +562,25 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   m->hblk_alt = m->hblk;
   for (auto& B : m->hblk_alt)
     for (int v = 0; v < kNState; ++v) std::swap(B.st[0][v], B.st[2][v]);
-  CK(cudaMalloc(&m->dblk, sizeof(DevBlock) * G.nb));
-  CK(cudaMalloc(&m->dblk_alt, sizeof(DevBlock) * G.nb));
-  CK(cudaMemcpyAsync(m->dblk, m->hblk.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(m->dblk_alt, m->hblk_alt.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice,
+  MCK(cudaMalloc(&m->dblk, sizeof(DevBlock) * G.nb));
+  MCK(cudaMalloc(&m->dblk_alt, sizeof(DevBlock) * G.nb));
+  MCK(cudaMemcpyAsync(m->dblk, m->hblk.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice, ctx->stream));
+  MCK(cudaMemcpyAsync(m->dblk_alt, m->hblk_alt.data(), sizeof(DevBlock) * G.nb, cudaMemcpyHostToDevice,
                      ctx->stream));
-  CK(cudaMalloc(&m->dred, 3 * sizeof(DevRed)));
-  CK(cudaMalloc(&m->dks, 3 * sizeof(KStage)));
+  MCK(cudaMalloc(&m->dred, 3 * sizeof(DevRed)));
+  MCK(cudaMalloc(&m->dks, 3 * sizeof(KStage)));
   if (G.dim == 3) {
     int rc = build_ec_maps(m);
     if (rc) { pmhd_gpu_mesh_destroy(m); return rc; }
   }
-  CK(cudaMalloc(&m->dctl, sizeof(DevCtl)));
-  CK(cudaMemsetAsync(m->dks, 0, 3 * sizeof(KStage), ctx->stream));
+  MCK(cudaMalloc(&m->dctl, sizeof(DevCtl)));
+  MCK(cudaMemsetAsync(m->dks, 0, 3 * sizeof(KStage), ctx->stream));
   if (const char* gr = std::getenv("PMHD_GRAPH")) m->graphs = std::atoi(gr) != 0 ? 1 : 0;
-  CK(cudaMallocHost(&m->hred, 3 * sizeof(DevRed)));
+  MCK(cudaMallocHost(&m->hred, 3 * sizeof(DevRed)));
   const size_t nrows = size_t(G.nb) * 5 * (G.ke - G.ks) * (G.je - G.js);
-  CK(cudaMalloc(&m->drows, nrows * sizeof(double)));
-  for (auto& e : m->ev) CK(cudaEventCreate(&e));
-  for (auto& e : m->ev_pre) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  MCK(cudaMalloc(&m->drows, nrows * sizeof(double)));
+  for (auto& e : m->ev) MCK(cudaEventCreate(&e));
+  for (auto& e : m->ev_pre) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // Overlap pays where the exchange is a real transfer (remote neighbours,
   // NCCL); with all neighbours local the exchange kernels take ~3 % of a
   // stage and splitting the flux launches costs more (measured -1.4 % at 256^3).
@@ -586,8 +597,8 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   if (G.mb[0] < G.ng) m->push_x1 = false;
   if (const char* px = std::getenv("PMHD_PUSH_X1")) m->push_x1 = m->push_x1 && std::atoi(px) != 0;
   m->slab_ev.resize((G.ke - G.ks) / 8 + 2);
-  for (auto& e : m->slab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  CK(cudaStreamSynchronize(ctx->stream));
+  for (auto& e : m->slab_ev) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  MCK(cudaStreamSynchronize(ctx->stream));
   *out = m;
   return PMHD_OK;
 }
