@@ -35,6 +35,16 @@ CASES = {
                         wave_n1=1, wave_n2=1, wave_amp=1e-3, riemann="roe"), 4),
     "ot2d_roe": (dict(nx1=64, nx2=64, nx3=1, mb1=32, mb2=64, mb3=1, pgen="orszag_tang", cfl=0.4,
                       riemann="roe"), 20),
+    # edge cases: ragged blocks (no tile divides them), ng = 3 / 4, tiny blocks
+    # (4 cells: the x1 ghost push ranges of both sides cover the whole block)
+    "wave3d_ng3_ragged": (dict(nx1=40, nx2=12, nx3=10, mb1=20, mb2=12, mb3=10, ng=3, x2max=0.3, x3max=0.25,
+                               wave_n1=1, wave_amp=1e-3), 3),
+    "wave3d_ng4_8blk": (dict(nx1=16, nx2=16, nx3=16, mb1=8, mb2=8, mb3=8, ng=4, wave_n1=1, wave_n2=1,
+                             wave_n3=1, wave_amp=1e-3), 3),
+    "wave3d_tiny_blocks": (dict(nx1=16, nx2=8, nx3=8, mb1=4, mb2=8, mb3=4, x2max=0.5, x3max=0.5, wave_n1=1,
+                                wave_amp=1e-3), 3),
+    "ot2d_ragged": (dict(nx1=48, nx2=40, nx3=1, mb1=24, mb2=20, mb3=1, x2max=40 / 48, pgen="orszag_tang",
+                         cfl=0.4), 6),
     # a larger shock problem: 64^3 blast in 8 blocks, floors active
     "blast3d_64_floor": (dict(nx1=64, nx2=64, nx3=64, mb1=32, mb2=32, mb3=32, x1min=-0.5, x1max=0.5,
                               x2min=-0.5, x2max=0.5, x3min=-0.5, x3max=0.5, pgen="blast",
