@@ -37,6 +37,15 @@ namespace {
 #define PMHD_FLUX_X1_FX 32  // x1 tiles: faces along i
 #endif
 constexpr int NTHR = 128;
+#ifndef PMHD_FLUX_CPASYNC
+#define PMHD_FLUX_CPASYNC 0  // 1: phase-1 stencil loads as cp.async into shared memory
+#endif
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 #ifndef PMHD_FLUX_FACE_UNROLL
 #define PMHD_FLUX_FACE_UNROLL 1  // 2: both faces of a thread in one unrolled body
 #endif
@@ -115,56 +124,27 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   }
 
   // ---- phase 1: load + cons_to_prim of the stencil cells into smem --------
-  // The loads of PMHD_P1_BATCH cells are issued before any is consumed
-  // (memory-level parallelism: up to BATCH x 11 loads in flight per thread).
-  constexpr int NB = (PMHD_P1_BATCH < TS::PER) ? PMHD_P1_BATCH : TS::PER;
-#pragma unroll
-  for (int p0 = 0; p0 < TS::PER; p0 += NB) {
-  double ub[NB][11];
-  int cid[NB];
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    const int p = p0 + q;
-    cid[q] = -1;
-    if (p >= TS::PER) continue;
-    const int c = threadIdx.x + p * NTHR;
+  // tile cell c -> its (k, j, i); false outside the block array
+  auto cell_ijk = [&](int c, int& i, int& j, int& k) {
     const int col = c % TS::NCOL, row = c / TS::NCOL;
-    int i, j, k;
     if (DIR == 0) { i = fi0 - 2 + col; j = fs0 + row; k = t3; }
     else if (DIR == 1) { i = fi0 + col; j = fs0 - 2 + row; k = t3; }
     else { i = fi0 + col; k = fs0 - 2 + row; j = t3; }
-    if (c < TS::NCELL && i >= 0 && i < G.n1 && j >= 0 && j < G.n2 && k >= 0 && k < G.n3) {
-      const int id = G.idx(k, j, i);
-      cid[q] = id;
-#pragma unroll
-      for (int v = 0; v < 5; ++v) ub[q][v] = __ldg(S[v] + id);
-      ub[q][5] = __ldg(S[5] + id);
-      ub[q][6] = __ldg(S[5] + id + 1);
-      ub[q][7] = __ldg(S[6] + id);
-      ub[q][8] = __ldg(S[6] + id + G.sx);
-      ub[q][9] = __ldg(S[7] + id);
-      ub[q][10] = __ldg(S[7] + id + G.sy);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    if (cid[q] < 0) continue;
-    const int p = p0 + q;
-    const int c = threadIdx.x + p * NTHR;
-    const int id = cid[q];
+    return c < TS::NCELL && i >= 0 && i < G.n1 && j >= 0 && j < G.n2 && k >= 0 && k < G.n3;
+  };
+  // cons_to_prim of tile cell c (block index id) from its 11 raw values (5
+  // conserved, then the face pairs b1f, b2f, b3f); writes the 7 rotated
+  // primitives to sw[.][c] (and the cell-centred E where this tile owns it)
+  auto finish = [&](int c, int id, const double* ub) {
     double u[5], bc[3], w[8];
 #pragma unroll
-    for (int v = 0; v < 5; ++v) u[v] = ub[q][v];
-    bc[0] = 0.5 * (ub[q][5] + ub[q][6]);
-    bc[1] = 0.5 * (ub[q][7] + ub[q][8]);
-    bc[2] = 0.5 * (ub[q][9] + ub[q][10]);
+    for (int v = 0; v < 5; ++v) u[v] = ub[v];
+    bc[0] = 0.5 * (ub[5] + ub[6]);
+    bc[1] = 0.5 * (ub[7] + ub[8]);
+    bc[2] = 0.5 * (ub[9] + ub[10]);
     const int fl = cons_to_prim(u, bc, ph, w, false);
-    // (k, j, i) of the cell from its tile position
-    const int col = c % TS::NCOL, row = c / TS::NCOL;
     int i, j, k;
-    if (DIR == 0) { i = fi0 - 2 + col; j = fs0 + row; k = t3; }
-    else if (DIR == 1) { i = fi0 + col; j = fs0 - 2 + row; k = t3; }
-    else { i = fi0 + col; k = fs0 - 2 + row; j = t3; }
+    cell_ijk(c, i, j, k);
     if ((fl & 4) && k >= G.ks && k < G.ke && j >= G.js && j < G.je && i >= G.is && i < G.ie) {
       const long long gi = (long long)B.c[0] * G.mb[0] + (i - G.is);
       const long long gj = (long long)B.c[1] * G.mb[1] + (j - G.js);
@@ -184,8 +164,78 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     }
 #pragma unroll
     for (int n = 0; n < 7; ++n) sw[n][c] = w[rot_var<DIR>(n)];
+  };
+#if PMHD_FLUX_CPASYNC
+  {
+    // every raw value of this thread's cells in flight at once without
+    // registers: cp.async into shared memory (conserved -> sp[0..4][c],
+    // faces -> sw[0..5][c]; both are free until phase 1 writes sw[.][c] of
+    // the same cell, from the same thread)
+    int cid[TS::PER];
+#pragma unroll
+    for (int p = 0; p < TS::PER; ++p) {
+      cid[p] = -1;
+      const int c = threadIdx.x + p * NTHR;
+      int i, j, k;
+      if (cell_ijk(c, i, j, k)) {
+        const int id = G.idx(k, j, i);
+        cid[p] = id;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) cp_async8(&sp[v][c], S[v] + id);
+        cp_async8(&sw[0][c], S[5] + id);
+        cp_async8(&sw[1][c], S[5] + id + 1);
+        cp_async8(&sw[2][c], S[6] + id);
+        cp_async8(&sw[3][c], S[6] + id + G.sx);
+        cp_async8(&sw[4][c], S[7] + id);
+        cp_async8(&sw[5][c], S[7] + id + G.sy);
+      }
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int p = 0; p < TS::PER; ++p) {
+      if (cid[p] < 0) continue;
+      const int c = threadIdx.x + p * NTHR;
+      double ub[11];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) ub[v] = sp[v][c];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) ub[5 + q] = sw[q][c];
+      finish(c, cid[p], ub);
+    }
   }
+#else
+  // The loads of PMHD_P1_BATCH cells are issued before any is consumed
+  // (memory-level parallelism: up to BATCH x 11 loads in flight per thread).
+  constexpr int NB = (PMHD_P1_BATCH < TS::PER) ? PMHD_P1_BATCH : TS::PER;
+#pragma unroll
+  for (int p0 = 0; p0 < TS::PER; p0 += NB) {
+    double ub[NB][11];
+    int cid[NB];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const int p = p0 + q;
+      cid[q] = -1;
+      if (p >= TS::PER) continue;
+      const int c = threadIdx.x + p * NTHR;
+      int i, j, k;
+      if (cell_ijk(c, i, j, k)) {
+        const int id = G.idx(k, j, i);
+        cid[q] = id;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) ub[q][v] = __ldg(S[v] + id);
+        ub[q][5] = __ldg(S[5] + id);
+        ub[q][6] = __ldg(S[5] + id + 1);
+        ub[q][7] = __ldg(S[6] + id);
+        ub[q][8] = __ldg(S[6] + id + G.sx);
+        ub[q][9] = __ldg(S[7] + id);
+        ub[q][10] = __ldg(S[7] + id + G.sy);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NB; ++q)
+      if (cid[q] >= 0) finish(threadIdx.x + (p0 + q) * NTHR, cid[q], ub[q]);
   }
+#endif
   __syncthreads();
   if (PROF && threadIdx.x == 0) tph[1] = clock64();
 
