@@ -40,12 +40,14 @@ constexpr int NTHR = 128;
 #ifndef PMHD_FLUX_CPASYNC
 #define PMHD_FLUX_CPASYNC 0  // 1: phase-1 stencil loads as cp.async into shared memory
 #endif
+#if PMHD_FLUX_CPASYNC
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
                "l"(gmem)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+#endif
 #ifndef PMHD_FLUX_FACE_UNROLL
 #define PMHD_FLUX_FACE_UNROLL 1  // 2: both faces of a thread in one unrolled body
 #endif
