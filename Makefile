@@ -35,7 +35,12 @@ $(LIB)/libpmhd_gpu_parity.so: $(GPU_DEPS)
 	$(NVCC) $(NVFLAGS) --fmad=false -DPMHD_PARITY -shared -o $@ $(GPU_SRCS)
 
 # GPU test helper (tests/cuda): checks the product build's division / sqrt
-testlib: $(LIB)/test/libpmhd_divsqrt_check.so
+testlib: $(LIB)/test/libpmhd_divsqrt_check.so $(LIB)/test/libpmhd_gpu_check.so
+
+# bounds-checked debug build of the product (tests/test_gpu_bounds.py)
+$(LIB)/test/libpmhd_gpu_check.so: $(GPU_DEPS)
+	@mkdir -p $(LIB)/test
+	$(NVCC) $(NVFLAGS) $(FASTDS) -DPMHD_BOUNDS_CHECK -shared -o $@ $(GPU_SRCS)
 
 $(LIB)/test/libpmhd_divsqrt_check.so: tests/cuda/divsqrt_check.cu $(GPUSRC)/physics.cuh
 	@mkdir -p $(LIB)/test

@@ -28,6 +28,21 @@ struct KGeom {
   __host__ __device__ int idx(int k, int j, int i) const { return k * sy + j * sx + i; }
 };
 
+// Bounds-checked debug build (-DPMHD_BOUNDS_CHECK, lib/test/libpmhd_gpu_check.so;
+// compute-sanitizer is not available on the GPU pool): every element index the
+// fused kernels and the exchange form into a block array must lie inside the
+// array's (n3+1) planes, else the kernel traps.
+#ifdef PMHD_BOUNDS_CHECK
+#define PMHD_CHECK_ID(G, id)                                                  \
+  do {                                                                        \
+    if ((unsigned)(id) >= (unsigned)(((G).n3 + 1) * (G).sy)) __trap();       \
+  } while (0)
+#else
+#define PMHD_CHECK_ID(G, id) \
+  do {                       \
+  } while (0)
+#endif
+
 struct DevBlock {
   // st[0] = u^n (current), st[1] = u^{n+1/2}, st[2] = u^{n+1} (next).  The
   // ABI keeps two device copies of the block table with st[0] and st[2]

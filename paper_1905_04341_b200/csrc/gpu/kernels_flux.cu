@@ -222,6 +222,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       int i, j, k;
       if (cell_ijk(c, i, j, k)) {
         const int id = G.idx(k, j, i);
+        PMHD_CHECK_ID(G, id + G.sy);
         cid[q] = id;
 #pragma unroll
         for (int v = 0; v < 5; ++v) ub[q][v] = __ldg(S[v] + id);
@@ -296,6 +297,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     else if (DIR == 1) { i = fi; j = fs; k = t3; }
     else { i = fi; k = fs; j = t3; }
     const int id = G.idx(k, j, i);
+    PMHD_CHECK_ID(G, id);
     const double bn = __ldg(S[5 + DIR] + id);
     double out[8];
     int fb;

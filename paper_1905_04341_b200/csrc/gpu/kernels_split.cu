@@ -377,6 +377,8 @@ __global__ void k_exchange(const DevBlock* __restrict__ blks, KGeom G, int sel, 
       nbs[l] = 0;
       int q, qs, nb, side;
       if (l < nl && exch_layer(G, B, DIR, v, l, &q, &qs, &nb, &side)) {
+        PMHD_CHECK_ID(G, at(qs));
+        PMHD_CHECK_ID(G, at(q));
         val[l] = exch_src(blks, B, DIR, side, nb, sel, v)[at(qs)];
         dst[l] = at(q);
         nbs[l] = 1;
@@ -388,6 +390,8 @@ __global__ void k_exchange(const DevBlock* __restrict__ blks, KGeom G, int sel, 
   } else {
     int q, qs, nb, side;
     if (!exch_layer(G, B, DIR, v, blockIdx.y, &q, &qs, &nb, &side)) return;
+    PMHD_CHECK_ID(G, at(qs));
+    PMHD_CHECK_ID(G, at(q));
     B.st[sel][v][at(q)] = exch_src(blks, B, DIR, side, nb, sel, v)[at(qs)];
   }
 }

@@ -156,8 +156,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
   double* const* PL = push ? blks[B.nbr[0][0]].st[ks.out_sel] : nullptr;
   double* const* PR = push ? blks[B.nbr[0][1]].st[ks.out_sel] : nullptr;
   auto push_cell = [&](int v, int i, int id, double val) {
-    if (i < G.is + G.ng) ST(PL[v] + id + G.mb[0], val);
-    if (i >= G.ie - G.ng) ST(PR[v] + id - G.mb[0], val);
+    if (i < G.is + G.ng) { PMHD_CHECK_ID(G, id + G.mb[0]); ST(PL[v] + id + G.mb[0], val); }
+    if (i >= G.ie - G.ng) { PMHD_CHECK_ID(G, id - G.mb[0]); ST(PR[v] + id - G.mb[0], val); }
   };
 
   // cell-centred E of plane kk (written by the last-direction flux kernel
@@ -169,6 +169,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       const int c = q % EX, r = q / EX;
       if (c > nx + 1 || r > ny + 1) continue;
       const int id = G.idx(kk, j0 - 1 + r, i0 - 1 + c);
+      PMHD_CHECK_ID(G, id);
       ec(0, sl)[r][c] = __ldg(B.ec[0] + id);
       ec(1, sl)[r][c] = __ldg(B.ec[1] + id);
       ec(2, sl)[r][c] = __ldg(B.ec[2] + id);
@@ -183,6 +184,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       const int c = q % UX, r = q / UX;
       if (c >= nx || r > ny) continue;
       const int id = G.idx(d3 ? kk : kb, j0 + r, i0 + c);
+      if (d3) PMHD_CHECK_ID(G, id - G.sy);
+      PMHD_CHECK_ID(G, id);
       double e;
       if (d3) {
         e = corner_emf(mode, X2[5][id], X2[5][id - sy], X3[6][id], X3[6][id - sx], X2[7][id],
@@ -216,6 +219,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       const int c = q % UX, r = q / UX;
       if (c >= nx || r >= ny) continue;
       const int id = G.idx(kk, j0 + r, i0 + c);
+      PMHD_CHECK_ID(G, id);
       const double v = Sb[7][id] - (c1 * (e2s[h][r][c + 1] - e2s[h][r][c]) -
                                     c2 * (e1s[h][r + 1][c] - e1s[h][r][c]));
       b3s[h][r][c] = v;
@@ -283,6 +287,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       const int c = q % (UX + 1), r = q / (UX + 1);
       if (c > nx || r > ny) continue;
       const int id = G.idx(k, j0 + r, i0 + c);
+      PMHD_CHECK_ID(G, id - G.sx);
       const int ec_c = c + 1, ec_r = r + 1;
       e3s[r][c] = corner_emf(mode, X1[5][id], X1[5][id - sx], X2[6][id], X2[6][id - 1], X1[7][id],
                              X1[7][id - sx], X2[7][id], X2[7][id - 1], ec(2, lo)[ec_r][ec_c],
@@ -306,8 +311,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
         const int i = i0 + c;
         if (!push || i != G.is) ST(Sout[5] + id, v);
         if (push) {
-          if (i > G.is && i <= G.is + G.ng) ST(PL[5] + id + G.mb[0], v);
-          if (i >= G.ie - G.ng) ST(PR[5] + id - G.mb[0], v);
+          if (i > G.is && i <= G.is + G.ng) { PMHD_CHECK_ID(G, id + G.mb[0]); ST(PL[5] + id + G.mb[0], v); }
+          if (i >= G.ie - G.ng) { PMHD_CHECK_ID(G, id - G.mb[0]); ST(PR[5] + id - G.mb[0], v); }
         }
       }
     }
@@ -345,6 +350,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       if (c < nx && r < ny) {
         const int i = i0 + c, j = j0 + r;
         const int id = G.idx(k, j, i);
+        PMHD_CHECK_ID(G, id + G.sy);
         double u[5];
 #pragma unroll
         for (int v = 0; v < 5; ++v) {

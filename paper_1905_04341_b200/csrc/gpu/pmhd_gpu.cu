@@ -27,10 +27,15 @@ using namespace pmhd_gpu;
 #ifndef PMHD_VARIANT
 #define PMHD_VARIANT "fused(flux x3 + update) [PMHD_KERNELS=split: one kernel per op]"
 #endif
-#ifdef PMHD_PARITY
-#define PMHD_BUILD_INFO PMHD_VARIANT "+parity(fmad=false)"
+#ifdef PMHD_BOUNDS_CHECK
+#define PMHD_CHECK_INFO "+bounds-check"
 #else
-#define PMHD_BUILD_INFO PMHD_VARIANT "+fma"
+#define PMHD_CHECK_INFO ""
+#endif
+#ifdef PMHD_PARITY
+#define PMHD_BUILD_INFO PMHD_VARIANT "+parity(fmad=false)" PMHD_CHECK_INFO
+#else
+#define PMHD_BUILD_INFO PMHD_VARIANT "+fma" PMHD_CHECK_INFO
 #endif
 
 struct pmhd_ctx {
