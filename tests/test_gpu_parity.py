@@ -179,6 +179,10 @@ def test_config_errors(gpu_available):
         GpuSolver(RunConfig(nx1=48, nx2=32, nx3=32, mb1=32, mb2=32, mb3=32))
     with pytest.raises(ConfigError):
         GpuSolver(RunConfig(nx1=16, nx2=16, nx3=16, mb1=16, mb2=16, mb3=16, ng=1))
+    # maximum size: a block array must stay below 2^31 doubles (32-bit kernel
+    # indexing) -- rejected before any device allocation
+    with pytest.raises(ConfigError, match="too large"):
+        GpuSolver(RunConfig(nx1=1300, nx2=1300, nx3=1300, mb1=1300, mb2=1300, mb3=1300))
 
 
 def test_unphysical_error_matches_oracle(gpu_available):
