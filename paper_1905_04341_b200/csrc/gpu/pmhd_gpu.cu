@@ -88,6 +88,7 @@ struct pmhd_mesh {
   bool push_x1 = false;           // update kernel writes the x1 ghosts (PMHD_PUSH_X1, default on when possible)
   std::vector<cudaEvent_t> slab_ev;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t xev[25] = {};        // host<->device transfer pipeline (one per staged array + 1)
   pmhd_region_times times{};
 };
 
@@ -586,6 +587,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   MCK(cudaMalloc(&m->drows, nrows * sizeof(double)));
   for (auto& e : m->ev) MCK(cudaEventCreate(&e));
   for (auto& e : m->ev_pre) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : m->xev) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // Overlap pays where the exchange is a real transfer (remote neighbours,
   // NCCL); with all neighbours local the exchange kernels take ~3 % of a
   // stage and splitting the flux launches costs more (measured -1.4 % at 256^3).
@@ -626,6 +628,7 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   for (auto& e : m->ev) if (e) cudaEventDestroy(e);
   for (auto& e : m->slab_ev) if (e) cudaEventDestroy(e);
   for (auto& e : m->ev_pre) if (e) cudaEventDestroy(e);
+  for (auto& e : m->xev) if (e) cudaEventDestroy(e);
   delete m;
   return PMHD_OK;
 }
@@ -639,18 +642,47 @@ int pmhd_gpu_block_dims(const pmhd_mesh* m, int n[3]) {
 // One array between a dense host buffer (e1 x e2 x e3, i fastest) and a
 // pitched block array, staged through a contiguous device buffer: one large
 // PCIe DMA (full speed from pinned memory) plus an HBM-speed repack kernel.
-static int xfer(pmhd_ctx* ctx, const KGeom& G, double* host, double* dev, double* stg, int e1,
-                int e2, int e3, bool to_host) {
-  const size_t bytes = size_t(e1) * e2 * e3 * sizeof(double);
-  if (to_host) {
-    launch_repack(stg, dev, G, e1, e2, e3, 1, ctx->stream);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(host, stg, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  } else {
-    CK(cudaMemcpyAsync(stg, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
-    launch_repack(stg, dev, G, e1, e2, e3, 0, ctx->stream);
-    CK(cudaGetLastError());
+// Host <-> device transfer of a block's arrays through dense staging buffers:
+// one PCIe DMA per array at full speed from pinned memory plus an HBM-speed
+// repack kernel (pitched <-> dense).  Each array gets its own staging buffer
+// (the block's 24 face-data arrays are free outside a stage), so the copies
+// run back to back on the copy stream (stream2) while the repack / Bcc
+// kernels run on the main stream, ordered per array by events.
+struct Xfer {
+  double* host;
+  const double* dev;  // pitched source / destination (kind 0), face array (kind 1: Bcc)
+  int e1, e2, e3;
+  int kind, comp;     // kind 1: face_to_center_b of component comp (download only)
+};
+
+static int xfer_pipelined(pmhd_mesh* m, DevBlock& B, const Xfer* it, int n, bool to_host) {
+  pmhd_ctx* ctx = m->ctx;
+  const KGeom& G = m->G;
+  if (n > 24) return fail(ctx, PMHD_ERR_INPUT, "too many staged arrays");
+  cudaStream_t s = ctx->stream, c = ctx->stream2;
+  // the staging buffers may still be in use by work already on the main stream
+  CK(cudaEventRecord(m->xev[24], s));
+  CK(cudaStreamWaitEvent(c, m->xev[24], 0));
+  for (int q = 0; q < n; ++q) {
+    double* stg = B.fx[q / 8][q % 8];
+    const size_t bytes = size_t(it[q].e1) * it[q].e2 * it[q].e3 * sizeof(double);
+    if (to_host) {
+      if (it[q].kind == 1) launch_bcc_dense(stg, it[q].dev, G, it[q].comp, s);
+      else launch_repack(stg, const_cast<double*>(it[q].dev), G, it[q].e1, it[q].e2, it[q].e3, 1, s);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(m->xev[q], s));
+      CK(cudaStreamWaitEvent(c, m->xev[q], 0));
+      CK(cudaMemcpyAsync(it[q].host, stg, bytes, cudaMemcpyDeviceToHost, c));
+    } else {
+      CK(cudaMemcpyAsync(stg, it[q].host, bytes, cudaMemcpyHostToDevice, c));
+      CK(cudaEventRecord(m->xev[q], c));
+      CK(cudaStreamWaitEvent(s, m->xev[q], 0));
+      launch_repack(stg, const_cast<double*>(it[q].dev), G, it[q].e1, it[q].e2, it[q].e3, 0, s);
+      CK(cudaGetLastError());
+    }
   }
+  CK(cudaStreamSynchronize(c));
+  CK(cudaStreamSynchronize(s));
   return PMHD_OK;
 }
 
@@ -664,16 +696,13 @@ int pmhd_gpu_upload_block(pmhd_mesh* m, int gid, const double* u, const double* 
   const KGeom& G = m->G;
   const size_t nc = size_t(G.n1) * G.n2 * G.n3;
   DevBlock& B = m->hblk[b];
-  double* stg = B.fx[0][0];  // face-data scratch: free outside a stage
   double* hu = const_cast<double*>(u);
-  int rc = PMHD_OK;
-  for (int v = 0; v < 5 && !rc; ++v) rc = xfer(ctx, G, hu + v * nc, B.st[0][v], stg, G.n1, G.n2, G.n3, false);
-  if (!rc) rc = xfer(ctx, G, const_cast<double*>(b1f), B.st[0][5], stg, G.n1 + 1, G.n2, G.n3, false);
-  if (!rc) rc = xfer(ctx, G, const_cast<double*>(b2f), B.st[0][6], stg, G.n1, G.n2 + 1, G.n3, false);
-  if (!rc) rc = xfer(ctx, G, const_cast<double*>(b3f), B.st[0][7], stg, G.n1, G.n2, G.n3 + 1, false);
-  if (rc) return rc;
-  CK(cudaStreamSynchronize(ctx->stream));
-  return PMHD_OK;
+  Xfer it[8];
+  for (int v = 0; v < 5; ++v) it[v] = {hu + v * nc, B.st[0][v], G.n1, G.n2, G.n3, 0, 0};
+  it[5] = {const_cast<double*>(b1f), B.st[0][5], G.n1 + 1, G.n2, G.n3, 0, 0};
+  it[6] = {const_cast<double*>(b2f), B.st[0][6], G.n1, G.n2 + 1, G.n3, 0, 0};
+  it[7] = {const_cast<double*>(b3f), B.st[0][7], G.n1, G.n2, G.n3 + 1, 0, 0};
+  return xfer_pipelined(m, B, it, 8, false);
 }
 
 int pmhd_gpu_download_block(pmhd_mesh* m, int gid, double* u, double* w, double* b1f, double* b2f,
@@ -685,30 +714,24 @@ int pmhd_gpu_download_block(pmhd_mesh* m, int gid, double* u, double* w, double*
   const KGeom& G = m->G;
   const size_t nc = size_t(G.n1) * G.n2 * G.n3;
   DevBlock& B = m->hblk[b];
-  double* stg = B.fx[0][0];
-  int rc = PMHD_OK;
+  Xfer it[24];
+  int n = 0;
   if (u) {
-    for (int v = 0; v < 5 && !rc; ++v) rc = xfer(ctx, G, u + v * nc, B.st[0][v], stg, G.n1, G.n2, G.n3, true);
+    for (int v = 0; v < 5; ++v) it[n++] = {u + v * nc, B.st[0][v], G.n1, G.n2, G.n3, 0, 0};
     // face_to_center_b on the device, same IEEE operations
-    for (int c = 0; c < 3 && !rc; ++c) {
-      launch_bcc_dense(stg, B.st[0][5 + c], G, c, ctx->stream);
-      CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(u + (5 + c) * nc, stg, nc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    }
+    for (int c = 0; c < 3; ++c) it[n++] = {u + (5 + c) * nc, B.st[0][5 + c], G.n1, G.n2, G.n3, 1, c};
   }
-  if (b1f && !rc) rc = xfer(ctx, G, b1f, B.st[0][5], stg, G.n1 + 1, G.n2, G.n3, true);
-  if (b2f && !rc) rc = xfer(ctx, G, b2f, B.st[0][6], stg, G.n1, G.n2 + 1, G.n3, true);
-  if (b3f && !rc) rc = xfer(ctx, G, b3f, B.st[0][7], stg, G.n1, G.n2, G.n3 + 1, true);
-  if (rc) return rc;
+  if (b1f) it[n++] = {b1f, B.st[0][5], G.n1 + 1, G.n2, G.n3, 0, 0};
+  if (b2f) it[n++] = {b2f, B.st[0][6], G.n1, G.n2 + 1, G.n3, 0, 0};
+  if (b3f) it[n++] = {b3f, B.st[0][7], G.n1, G.n2, G.n3 + 1, 0, 0};
   if (w) {
-    rc = reset_red(m);
+    int rc = reset_red(m);
     if (rc) return rc;
     launch_c2p_all(m->dblk, G, m->ph, 0, m->dred, 0, ctx->stream);
-    for (int v = 0; v < 8 && !rc; ++v) rc = xfer(ctx, G, w + v * nc, B.w[v], stg, G.n1, G.n2, G.n3, true);
-    if (rc) return rc;
+    CK(cudaGetLastError());
+    for (int v = 0; v < 8; ++v) it[n++] = {w + v * nc, B.w[v], G.n1, G.n2, G.n3, 0, 0};
   }
-  CK(cudaStreamSynchronize(ctx->stream));
-  return PMHD_OK;
+  return xfer_pipelined(m, B, it, n, true);
 }
 
 int pmhd_gpu_exchange(pmhd_mesh* m) {
