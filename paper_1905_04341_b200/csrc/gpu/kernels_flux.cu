@@ -61,9 +61,12 @@ constexpr int kFaceUnroll = PMHD_FLUX_FACE_UNROLL;
 #ifndef PMHD_FLUX_MINB
 #define PMHD_FLUX_MINB 5
 #endif
+#ifndef PMHD_FLUX_MINB_ROE
+#define PMHD_FLUX_MINB_ROE 4
+#endif
 template <int RS>
 struct FluxMinB {
-  static constexpr int value = (RS == PMHD_RIEMANN_ROE) ? 4 : PMHD_FLUX_MINB;
+  static constexpr int value = (RS == PMHD_RIEMANN_ROE) ? PMHD_FLUX_MINB_ROE : PMHD_FLUX_MINB;
 };
 
 template <int DIR>
@@ -301,7 +304,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     const double bn = __ldg(S[5 + DIR] + id);
     double out[8];
     int fb;
-    if constexpr (PMHD_FLUX_SMEMW && RS == PMHD_RIEMANN_HLLD) {
+    if constexpr (PMHD_FLUX_SMEMW && (RS == PMHD_RIEMANN_HLLD || RS == PMHD_RIEMANN_ROE)) {
       const SmemW wl{wsrc + cl, TS::NCELL}, wr{&sw[0][0] + ch, TS::NCELL};
       fb = face_solve<RS>(wl, wr, bn, ph, c1024, out);
     } else {
