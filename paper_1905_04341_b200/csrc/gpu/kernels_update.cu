@@ -13,6 +13,8 @@
 // faces, which only the owner writes back), then updates and re-primitivises
 // its cells.  Outputs go to a separate buffer (st[out_sel]), so tiles that
 // recompute a shared face never read a value another tile has overwritten.
+#include <atomic>
+
 #include "kernels.cuh"
 
 namespace pmhd_gpu {
@@ -436,14 +438,16 @@ void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, 
   constexpr int smem = (int)sizeof(UpdSmem) + 128;  // + alignment slack
 #define PMHD_UPDATE_LAUNCH(SG)                                                                          \
   do {                                                                                                  \
-    static unsigned long long attr_devs = 0; /* (per device: the attribute is per-device state) */    \
+    /* per device (the attribute is per-device state); atomic: contexts may  \
+       live on different host threads; setting it twice is harmless */       \
+    static std::atomic<unsigned long long> attr_devs{0};                                                \
     int dev = 0;                                                                                        \
     cudaGetDevice(&dev);                                                                                \
-    if (!(attr_devs & (1ULL << (dev & 63)))) {                                                          \
+    if (!(attr_devs.load() & (1ULL << (dev & 63)))) {                                                   \
       cudaFuncSetAttribute(k_update_fused<SG, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
       cudaFuncSetAttribute(k_update_fused<SG, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
       cudaFuncSetAttribute(k_update_fused<SG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);   \
-      attr_devs |= 1ULL << (dev & 63);                                                                  \
+      attr_devs.fetch_or(1ULL << (dev & 63));                                                           \
     }                                                                                                   \
     if (kd)                                                                                             \
       k_update_fused<SG, 2><<<grid, UTHR, smem, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, ec_maps, push);      \
