@@ -14,7 +14,9 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -Xlinker -Bsymbolic -std=c++17 -Xcompiler -fPI
             -Xptxas -warn-spills --expt-relaxed-constexpr
 HOSTFLAGS:= -std=c++20 -O2 -march=x86-64-v3 -fPIC -Wall -Wextra -Iinclude
 GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu $(GPUSRC)/kernels_flux.cu $(GPUSRC)/kernels_update.cu $(GPUSRC)/kernels_halo.cu $(GPUSRC)/kernels_drive.cu $(GPUSRC)/kernels_ctl.cu
-FASTDS   := -DPMHD_FAST_DIVSQRT
+# product division / sqrt: MUFU seed + one cubic Newton step, within 1 ulp
+# (tests/test_divsqrt.py); -DPMHD_FAST_DIVSQRT alone is the IEEE-exact variant
+FASTDS   := -DPMHD_FAST_DIVSQRT -DPMHD_DIVSQRT_1ULP
 GPU_DEPS := $(GPU_SRCS) $(wildcard $(GPUSRC)/*.cuh) include/pmhd_gpu.h Makefile
 
 all: host gpu cli oracle testlib
@@ -35,14 +37,19 @@ $(LIB)/libpmhd_gpu_parity.so: $(GPU_DEPS)
 	$(NVCC) $(NVFLAGS) --fmad=false -DPMHD_PARITY -shared -o $@ $(GPU_SRCS)
 
 # GPU test helper (tests/cuda): checks the product build's division / sqrt
-testlib: $(LIB)/test/libpmhd_divsqrt_check.so $(LIB)/test/libpmhd_gpu_check.so
+testlib: $(LIB)/test/libpmhd_divsqrt_check.so $(LIB)/test/libpmhd_divsqrt_exact_check.so \
+         $(LIB)/test/libpmhd_gpu_check.so
+
+$(LIB)/test/libpmhd_divsqrt_exact_check.so: tests/cuda/divsqrt_check.cu $(GPUSRC)/physics.cuh Makefile
+	@mkdir -p $(LIB)/test
+	$(NVCC) $(NVFLAGS) -DPMHD_FAST_DIVSQRT -shared -o $@ $<
 
 # bounds-checked debug build of the product (tests/test_gpu_bounds.py)
 $(LIB)/test/libpmhd_gpu_check.so: $(GPU_DEPS)
 	@mkdir -p $(LIB)/test
 	$(NVCC) $(NVFLAGS) $(FASTDS) -DPMHD_BOUNDS_CHECK -shared -o $@ $(GPU_SRCS)
 
-$(LIB)/test/libpmhd_divsqrt_check.so: tests/cuda/divsqrt_check.cu $(GPUSRC)/physics.cuh
+$(LIB)/test/libpmhd_divsqrt_check.so: tests/cuda/divsqrt_check.cu $(GPUSRC)/physics.cuh Makefile
 	@mkdir -p $(LIB)/test
 	$(NVCC) $(NVFLAGS) $(FASTDS) -shared -o $@ $<
 

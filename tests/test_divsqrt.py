@@ -1,7 +1,11 @@
-"""The product build's branch-free division / square root (physics.cuh,
-PMHD_FAST_DIVSQRT) against the IEEE operators, bit for bit, over operands
-spanning the ranges the physics produces (and well beyond): 1e-30 .. 1e30,
-both signs, exact squares, powers of two, and sqrt(0)."""
+"""The product build's branch-free division / square root (physics.cuh) against
+the IEEE operators over operands spanning the ranges the physics produces (and
+well beyond): 1e-30 .. 1e30, both signs, exact squares, powers of two, and
+sqrt(0).
+
+* product variant (PMHD_DIVSQRT_1ULP, the Makefile's FASTDS): MUFU seed + one
+  cubic Newton step, no rounding correction -- every result within 1 ulp;
+* PMHD_FAST_DIVSQRT alone: the IEEE fast-path sequence -- bit for bit."""
 import ctypes as C
 
 import numpy as np
@@ -12,16 +16,12 @@ from paper_1905_04341_b200.native import LIB_DIR
 pytestmark = pytest.mark.gpu
 
 
-def _lib():
-    path = LIB_DIR / "test" / "libpmhd_divsqrt_check.so"
+def _run(name):
+    path = LIB_DIR / "test" / name
     if not path.exists():
         pytest.fail(f"missing {path} (run __graft_entry__.build())")
     L = C.CDLL(str(path))
     L.pmhd_test_divsqrt.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]
-    return L
-
-
-def test_fast_divsqrt_bitwise_ieee(gpu_available):
     rng = np.random.default_rng(1905)
     n = 1 << 22
     a = rng.choice([-1.0, 1.0], n) * 10.0 ** rng.uniform(-30, 30, n)
@@ -32,8 +32,20 @@ def test_fast_divsqrt_bitwise_ieee(gpu_available):
     a[n // 4: n // 4 + 1000] = np.arange(1000, dtype=np.float64) ** 2
     b[n // 4: n // 4 + 1000] = 2.0 ** rng.integers(-60, 60, 1000)
     a[n // 4] = 0.0
-    out = np.zeros(2, dtype=np.uint64)
-    rc = _lib().pmhd_test_divsqrt(a.ctypes.data, b.ctypes.data, n, out.ctypes.data)
+    out = np.zeros(4, dtype=np.uint64)
+    rc = L.pmhd_test_divsqrt(a.ctypes.data, b.ctypes.data, n, out.ctypes.data)
     assert rc == 0
+    return out
+
+
+def test_product_divsqrt_within_one_ulp(gpu_available):
+    out = _run("libpmhd_divsqrt_check.so")
+    assert out[2] <= 1, f"division off by {out[2]} ulp"
+    assert out[3] <= 1, f"sqrt off by {out[3]} ulp"
+    print(f"product variant: {out[0]} divisions and {out[1]} square roots differ from IEEE, by <= 1 ulp")
+
+
+def test_exact_divsqrt_bitwise_ieee(gpu_available):
+    out = _run("libpmhd_divsqrt_exact_check.so")
     assert out[0] == 0, f"{out[0]} divisions differ from IEEE"
     assert out[1] == 0, f"{out[1]} square roots differ from IEEE"
