@@ -32,10 +32,15 @@ using namespace pmhd_gpu;
 #else
 #define PMHD_CHECK_INFO ""
 #endif
+#if defined(PMHD_DIVSQRT_1ULP) && !defined(PMHD_PARITY)
+#define PMHD_DS_INFO "+divsqrt(1ulp)"
+#else
+#define PMHD_DS_INFO ""
+#endif
 #ifdef PMHD_PARITY
 #define PMHD_BUILD_INFO PMHD_VARIANT "+parity(fmad=false)" PMHD_CHECK_INFO
 #else
-#define PMHD_BUILD_INFO PMHD_VARIANT "+fma" PMHD_CHECK_INFO
+#define PMHD_BUILD_INFO PMHD_VARIANT "+fma" PMHD_DS_INFO PMHD_CHECK_INFO
 #endif
 
 struct pmhd_ctx {
