@@ -1,3 +1,6 @@
+#!/bin/bash
+# Turbulence-driving session: driven parity tests (GPU and gloo), the 512^3
+# decaying / driven CLI benches, and the ncu launch list of one driving event.
 set -x
 python -m pytest tests/test_gpu_parity.py -q -x -k "driven or drive" 2>&1 | tail -3
 python -m pytest tests/test_drive.py tests/test_parallel_cpu.py -q -x -k driven 2>&1 | tail -2

@@ -1,3 +1,6 @@
+#!/bin/bash
+# Round-end check: GPU tests, both bench arms (default args) and the CLI
+# configs; outputs under gpurun_out/.
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err

@@ -1,3 +1,6 @@
+#!/bin/bash
+# Roe A/B: GPU tests, then the bench with --riemann roe for the base / default /
+# 5-CTA builds (lib/exp), and the Roe parity tests against the 5-CTA build.
 L=paper_1905_04341_b200/lib
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
 B="python bench.py --steps 6 --warmup 3 --no-cpu-baseline --no-e2e"
