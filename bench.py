@@ -48,6 +48,9 @@ def parse():
                    help="MeshBlock edge (default = --size: one block per GPU; 128 with --size 256: the "
                         "8-blocks-per-GPU M4 variant)")
     p.add_argument("--riemann", default="hlld")
+    p.add_argument("--workload", choices=["m4", "m5"], default="m4",
+                   help="m4: linear wave, --size^3 cells per GPU (weak scaling, the default and the headline); "
+                        "m5: decaying turbulence 512^3 in 128^3 MeshBlocks split over the ranks (strong scaling)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -84,6 +87,17 @@ def make_config(n, ranks, riemann="hlld", nz=None, block=0):
     return RunConfig(nx1=n * p[0], nx2=n * p[1], nx3=nz * p[2], mb1=mb, mb2=mb, mb3=min(mb, nz), x1max=float(p[0]),
                      x2max=float(p[1]), x3max=p[2] * nz / n, wave_mode=6, wave_amp=1e-6, cfl=0.3,
                      riemann=riemann)
+
+
+def make_m5_config(riemann="hlld", nz=None):
+    """M5 (BASELINE config 5): 512^3 decaying turbulence in 128^3 MeshBlocks,
+    examples/turbulence_512.in (nz: the CPU legs' bounded 512 x 512 x nz slab)."""
+    from paper_1905_04341_b200 import RunConfig
+    text = open(os.path.join(ROOT, "examples", "turbulence_512.in")).read()
+    kw = dict(riemann=riemann)
+    if nz is not None:
+        kw.update(nx3=nz, mb3=nz, x3max=nz / 512.0)
+    return RunConfig(text, **kw)
 
 
 def falg():
@@ -192,14 +206,14 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def cpu_oracle_cups(n, cycles_max, seconds, workers, nz=32):
+def cpu_oracle_cups(n, cycles_max, seconds, workers, nz=32, workload="m4"):
     """The oracle (test infrastructure) on a bounded sample of the workload:
     the 256 x 256 x nz periodic slab of the M4 linear wave (same per-cell
     work).  Dispatched through the reference's own par_for / ThreadPool
     (oracle/_ref) when that build is present."""
     from oracle.binding import OracleSolver
     ref = os.path.exists(os.path.join(ROOT, "oracle", "_ref", "liboracle_ref.so"))
-    cfg = make_config(n, 1, nz=nz)
+    cfg = make_config(n, 1, nz=nz) if workload == "m4" else make_m5_config(nz=nz)
     s = OracleSolver(cfg, workers=workers, ref=ref)
     s.load_pgen()
     dt = s.new_dt()
@@ -216,8 +230,9 @@ def cpu_oracle_cups(n, cycles_max, seconds, workers, nz=32):
     per = [cells / t for t in times]
     return {"value": cells * len(times) / sum(times), "p80": sorted(per)[int(0.8 * (len(per) - 1))],
             "unit": "cell-updates/s", "cores": workers, "kind": "port",
-            "sample": f"{len(times)} VL2 cycle(s) of the {n}x{n}x{nz} periodic slab of the M4 linear wave "
-                      f"(same per-cell work as 256^3), oracle/{'_ref (reference par_for/ThreadPool, SimdNested)' if ref else 'liboracle.so'}, "
+            "sample": f"{len(times)} VL2 cycle(s) of the {cfg.desc.nx[0]}x{cfg.desc.nx[1]}x{nz} periodic slab of the "
+                      f"{'M4 linear wave' if workload == 'm4' else 'M5 turbulence'} "
+                      f"(same per-cell work as the full mesh), oracle/{'_ref (reference par_for/ThreadPool, SimdNested)' if ref else 'liboracle.so'}, "
                       f"{workers} worker threads"}
 
 
@@ -229,7 +244,10 @@ def run_reference(args):
     from oracle.binding import OracleSolver
     ref = os.path.exists(os.path.join(ROOT, "oracle", "_ref", "liboracle_ref.so"))
     nz = 32
-    cfg = make_config(args.size, 1, riemann=args.riemann, nz=nz)
+    if args.workload == "m4":
+        cfg = make_config(args.size, 1, riemann=args.riemann, nz=nz)
+    else:
+        cfg = make_m5_config(riemann=args.riemann, nz=nz)
     s = OracleSolver(cfg, workers=workers, ref=ref)
     s.load_pgen()
     dt = s.new_dt()
@@ -243,14 +261,19 @@ def run_reference(args):
     cells = cfg.active_cells
     tot = sum(times)
     value = cells * len(times) / tot
-    sample = (f"each step = 1 VL2 cycle of the {args.size}x{args.size}x{nz} periodic slab of the M4 linear wave "
-              f"(bounded sample of the 256^3 workload; identical per-cell work), CPU oracle "
+    wl = "M4 linear wave" if args.workload == "m4" else "M5 turbulence"
+    sample = (f"each step = 1 VL2 cycle of the {cfg.desc.nx[0]}x{cfg.desc.nx[1]}x{nz} periodic slab of the {wl} "
+              f"(bounded sample of the workload; identical per-cell work), CPU oracle "
               f"{'through the reference par_for/ThreadPool (oracle/_ref)' if ref else '(oracle/liboracle.so)'}")
     line = {"impl": "reference", "metric": "cell-updates/s (fp64 VL2+PLM+HLLD+CT MHD)", "value": value,
             "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (linear-wave problem generator)",
-            "config": {"workload": f"M4 linear fast wave {args.size}^3 per GPU (sampled as {args.size}x{args.size}x{nz})",
+            "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+            "scaling": "weak" if args.workload == "m4" else "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic ({'linear-wave' if args.workload == 'm4' else 'turbulence'} problem generator)",
+            "config": {"workload": (f"M4 linear fast wave {args.size}^3 per GPU (sampled as {args.size}x{args.size}x{nz})"
+                                    if args.workload == "m4" else
+                                    f"M5 decaying turbulence 512^3, 128^3 MeshBlocks (sampled as 512x512x{nz})"),
                        "riemann": args.riemann, "cells_per_step": cells},
             "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": workers, "kind": "port",
                              "sample": sample},
@@ -281,8 +304,12 @@ def run_ours(args):
     n = args.size
     # (p1 n) x (p2 n) x (p3 n) periodic mesh, n^3 cells per rank (one block,
     # or --block edge blocks)
-    cfg = make_config(n, ws, riemann=args.riemann, block=args.block)
-    cells_rank = n ** 3
+    if args.workload == "m4":
+        cfg = make_config(n, ws, riemann=args.riemann, block=args.block)
+        cells_rank = n ** 3
+    else:  # M5: one fixed 512^3 mesh, its 64 blocks split over the ranks
+        cfg = make_m5_config(riemann=args.riemann)
+        cells_rank = cfg.active_cells // ws
     from paper_1905_04341_b200.parallel import plan_for, DistributedVL2, TorchDistTransport
     plan = plan_for(cfg, ws)
     my_gids = plan.local_gids(rank)
@@ -373,7 +400,8 @@ def run_ours(args):
     flux_ms = (rt["c2p_ms"] + rt["reconstruct_ms"] + rt["riemann_ms"]) / nprof / n_flux
     flux_flops = F_flux * cells_rank / n_flux              # algorithmic flops per launch
     flux_tf = flux_flops / (flux_ms * 1e-3) / 1e12
-    tr = ncu_traffic() if args.size == 256 and dim == 3 else None
+    tr = (ncu_traffic() if args.workload == "m4" and args.size == 256 and dim == 3 and args.block in (0, 256)
+          else None)
     upd_ms = (rt["ct_emf_ms"] + rt["integrate_ms"]) / nprof / 2  # update kernel = ct_emf + integrate regions
     roofline = {
         "bound": "fp64", "achieved": flux_tf, "peak": fp64_pk, "unit": "TFLOP/s",
@@ -444,22 +472,30 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_cups(n, 5, args.cpu_seconds, os.cpu_count() or 1)
+        cpu = cpu_oracle_cups(n, 5, args.cpu_seconds, os.cpu_count() or 1, workload=args.workload)
 
+    # 8 doubles of state per cell incl. ghosts
+    state_bytes = 64 * cells_rank * ((cfg.desc.mb[0] + 2 * cfg.desc.ng) / cfg.desc.mb[0]) ** 3
     if rank == 0:
         line = {
             "metric": "cell-updates/s (fp64 VL2+PLM+HLLD+CT MHD)", "value": value,
             "unit": "cell-updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (linear-wave problem generator)",
+            "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.workload == "m4" else "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic ({'linear-wave' if args.workload == 'm4' else 'turbulence'} problem generator)",
             "config": {"workload": (f"M4 3D linear fast wave, {n}^3 active cells per GPU in "
                                     f"{len(my_gids)} MeshBlock(s) of {cfg.desc.mb[0]}^3, "
-                                    f"HLLD+PLM(MC)+CT, CFL 0.3, A=1e-6"),
-                       "global_cells": [n * q for q in rank_grid(ws)],
+                                    f"HLLD+PLM(MC)+CT, CFL 0.3, A=1e-6" if args.workload == "m4" else
+                                    f"M5 decaying turbulence 512^3 in 128^3 MeshBlocks, {len(my_gids)} per GPU "
+                                    f"(strong scaling), HLLD+PLM(MC)+CT"),
+                       "global_cells": ([n * q for q in rank_grid(ws)] if args.workload == "m4" else
+                                        list(cfg.desc.nx)),
                        "parallelism": (f"{ws} rank(s) as a {'x'.join(map(str, rank_grid(ws)))} grid of {n}^3 "
-                                       f"bricks, one per rank"),
-                       "l2": (f"inputs larger than L2 ({8 * 8 * (n + 4) ** 3 / 1e9:.2f} GB state per GPU "
-                              f"vs 126 MB L2)" if 64 * (n + 4) ** 3 > 126e6 else
+                                       f"bricks, one per rank" if args.workload == "m4" else
+                                       f"{ws} rank(s), {len(my_gids)} of the 64 blocks each (compact bricks)"),
+                       "l2": (f"inputs larger than L2 ({state_bytes / 1e9:.2f} GB state per GPU "
+                              f"vs 126 MB L2)" if state_bytes > 126e6 else
                               "state smaller than L2 (small validation size)"),
                        "statistic": "value = mean over K cycles; p80 in extra.p80_cups",
                        "variant": g.build_info},
