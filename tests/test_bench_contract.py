@@ -21,9 +21,12 @@ def run_bench(*args, timeout=600):
     return json.loads(lines[0])
 
 
-def test_reference_arm_line():
-    d = run_bench("--impl", "reference", "--size", "32", "--steps", "1", "--warmup", "0")
+@pytest.mark.parametrize("workload", ["m4", "m5"])
+def test_reference_arm_line(workload):
+    extra = ["--size", "32"] if workload == "m4" else []
+    d = run_bench("--impl", "reference", "--workload", workload, *extra, "--steps", "1", "--warmup", "0")
     assert BASE <= set(d)
+    assert d["scaling"] == ("weak" if workload == "m4" else "strong")
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["dtype"] == "f64" and d["config"]["workload"]
     cb = d["cpu_baseline"]
