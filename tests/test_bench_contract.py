@@ -47,3 +47,21 @@ def test_our_arm_line(gpu_available):
     assert e["value"] < d["value"]  # host copies inside the timed region
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_weak_scaling_rank_grid():
+    """bench.py's M4 decomposition is SURVEY.md §8d's (p1,p2,p3) rank grid,
+    one n^3 block per rank; M5 splits its 64 blocks into equal bricks."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1905_04341_b200.parallel import plan_for
+    for ranks, grid in [(1, [1, 1, 1]), (2, [2, 1, 1]), (4, [2, 2, 1]), (8, [2, 2, 2])]:
+        assert bench.rank_grid(ranks) == grid
+        cfg = bench.make_config(64, ranks)
+        assert list(cfg.desc.nx) == [64 * g for g in grid] and cfg.nblocks == ranks
+        plan = plan_for(cfg, ranks)
+        assert sorted(g for r in range(ranks) for g in plan.local_gids(r)) == list(range(ranks))
+        assert all(len(plan.local_gids(r)) == 1 for r in range(ranks))
+        m5 = bench.make_m5_config()
+        p5 = plan_for(m5, ranks)
+        assert all(len(p5.local_gids(r)) == 64 // ranks for r in range(ranks))
