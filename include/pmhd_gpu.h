@@ -14,7 +14,12 @@
  * point below names the reference op it replaces.
  *
  * Conventions
- *  - All arithmetic is IEEE fp64 (Real=double, defs.hpp:16).
+ *  - All arithmetic is fp64 (Real=double, defs.hpp:16).  The parity library
+ *    (libpmhd_gpu_parity.so) uses IEEE operations in the oracle's order and
+ *    is bit-identical to the CPU oracle.  The product library
+ *    (libpmhd_gpu.so) contracts multiply-adds into FMAs and forms division
+ *    and square root within 1 ulp of the IEEE result (INTEGRATION.md
+ *    section 4); its fields stay within 1e-11 per cell of the oracle.
  *  - Host arrays are exactly the reference layout (array.hpp:19-80): k-j-i
  *    order with i fastest; the conserved array is variable-major with
  *    NCONS=8 variables (rho,m1,m2,m3,E,Bcc1,Bcc2,Bcc3; defs.hpp:22).  Block

@@ -409,10 +409,34 @@ int finish(pmhd_mesh* m, int stage_lo, int stage_hi, double* dt_next, pmhd_statu
   return PMHD_OK;
 }
 
+// A pending stage prefetch (interior flux tiles on stream2) writes the
+// face-data arrays the transfers stage through and accumulates into the
+// reduction slots: the main stream waits for it, and its fluxes are void
+// afterwards (the next stage recomputes every tile).
+int drop_prefetch(pmhd_mesh* m) {
+  pmhd_ctx* ctx = m->ctx;
+  if (m->prefetched) {
+    CK(cudaStreamWaitEvent(ctx->stream, m->ev_pre[1], 0));
+    m->prefetched = 0;
+  }
+  return PMHD_OK;
+}
+
 int local_index(const pmhd_mesh* m, int gid) {
   for (size_t b = 0; b < m->gids.size(); ++b)
     if (m->gids[b] == gid) return int(b);
   return -1;
+}
+
+// Empty kernel: cudaFuncGetAttributes on it fails unless this library's
+// sm_100a image loads on the device (pmhd_gpu_ctx_create).
+__global__ void k_image_probe() {}
+
+// Every ABI call that touches the device makes the context's device current
+// first: the caller may have switched devices between calls.
+int use_device(pmhd_ctx* ctx) {
+  CK(cudaSetDevice(ctx->device));
+  return PMHD_OK;
 }
 
 }  // namespace
@@ -430,7 +454,17 @@ int pmhd_gpu_ctx_create(int device, pmhd_ctx** out) {
   if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) return PMHD_ERR_CUDA;
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return PMHD_ERR_CUDA;
-  if (prop.major != 10) return PMHD_ERR_CUDA;  // built for sm_100a only
+  // built for sm_100a only: arch-specific code loads on compute capability
+  // 10.0 alone, so a 10.x part other than 10.0 is refused here rather than
+  // at the first launch ("no kernel image"); the probe confirms the image
+  // loads on this device
+  if (prop.major != 10 || prop.minor != 0) return PMHD_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return PMHD_ERR_CUDA;
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_image_probe) != cudaSuccess) {
+    cudaGetLastError();
+    return PMHD_ERR_CUDA;
+  }
   auto* ctx = new pmhd_ctx;
   ctx->device = device;
   if (cudaSetDevice(device) != cudaSuccess ||
@@ -486,6 +520,24 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
     }
     G.sx = int(sx);
     G.sy = int(sy);
+  }
+  {
+    // every kernel serves all local blocks in one launch with the block index
+    // folded into gridDim.z together with at most n+1 planes or rows of a
+    // block (flux: face planes / rows, update: k segments, split kernels and
+    // exchange: planes or 8 arrays); gridDim.z is limited to 65535
+    const long long nbl = (n_local <= 0 || !gids)
+                              ? (long long)(desc->nx[0] / desc->mb[0]) * (desc->nx[1] / desc->mb[1]) *
+                                    (desc->nx[2] / desc->mb[2])
+                              : n_local;
+    const long long per = std::max({(long long)G.n2, (long long)G.n3, (long long)kNState}) + 1;
+    if (nbl * per > 65535) {
+      delete m;
+      return fail(ctx, PMHD_ERR_CONFIG,
+                  "too many MeshBlocks on this rank for their size: (local blocks) x (block cells incl. ghosts "
+                  "along x2/x3 + 1) must be <= 65535 (" + std::to_string(nbl) + " x " + std::to_string(per) +
+                      "); use larger MeshBlocks or more ranks");
+    }
   }
   G.is = G.ng; G.ie = G.ng + G.mb[0];
   G.js = G.ng; G.je = G.ng + G.mb[1];
@@ -694,10 +746,12 @@ static int xfer_pipelined(pmhd_mesh* m, DevBlock& B, const Xfer* it, int n, bool
 int pmhd_gpu_upload_block(pmhd_mesh* m, int gid, const double* u, const double* b1f,
                           const double* b2f, const double* b3f) {
   if (!m) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
   const int b = local_index(m, gid);
   if (b < 0) return fail(ctx, PMHD_ERR_INPUT, "block not local");
   if (!u || !b1f || !b2f || !b3f) return fail(ctx, PMHD_ERR_BUFFER, "null buffer");
+  if (int rc = drop_prefetch(m)) return rc;
   const KGeom& G = m->G;
   const size_t nc = size_t(G.n1) * G.n2 * G.n3;
   DevBlock& B = m->hblk[b];
@@ -713,9 +767,11 @@ int pmhd_gpu_upload_block(pmhd_mesh* m, int gid, const double* u, const double* 
 int pmhd_gpu_download_block(pmhd_mesh* m, int gid, double* u, double* w, double* b1f, double* b2f,
                             double* b3f) {
   if (!m) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
   const int b = local_index(m, gid);
   if (b < 0) return fail(ctx, PMHD_ERR_INPUT, "block not local");
+  if (int rc = drop_prefetch(m)) return rc;
   const KGeom& G = m->G;
   const size_t nc = size_t(G.n1) * G.n2 * G.n3;
   DevBlock& B = m->hblk[b];
@@ -741,8 +797,10 @@ int pmhd_gpu_download_block(pmhd_mesh* m, int gid, double* u, double* w, double*
 
 int pmhd_gpu_exchange(pmhd_mesh* m) {
   if (!m) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
   if (!m->all_local) return fail(ctx, PMHD_ERR_INPUT, "exchange needs all neighbours local");
+  if (int rc = drop_prefetch(m)) return rc;
   launch_exchange(m->dblk, m->G, 0, ctx->stream);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->stream));
@@ -751,7 +809,9 @@ int pmhd_gpu_exchange(pmhd_mesh* m) {
 
 int pmhd_gpu_new_dt(pmhd_mesh* m, double* dt_out, pmhd_status* st) {
   if (!m || !dt_out) return PMHD_ERR_INPUT;
-  int rc = reset_red(m);
+  if (int rc_ = use_device(m->ctx)) return rc_;
+  int rc = drop_prefetch(m);
+  if (!rc) rc = reset_red(m);
   if (rc) return rc;
   launch_dt_from_state(m->dblk, m->G, m->ph, m->dred, m->ctx->stream);
   return finish(m, 0, 0, dt_out, st);
@@ -759,6 +819,7 @@ int pmhd_gpu_new_dt(pmhd_mesh* m, double* dt_out, pmhd_status* st) {
 
 int pmhd_gpu_stage(pmhd_mesh* m, int stage, double dt, double* dt_next, pmhd_status* st) {
   if (!m) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   if (stage != 1 && stage != 2) return fail(m->ctx, PMHD_ERR_INPUT, "stage must be 1 or 2");
   if (!m->all_local) return fail(m->ctx, PMHD_ERR_INPUT, "stage needs all neighbours local");
   int rc = reset_red(m);
@@ -769,6 +830,7 @@ int pmhd_gpu_stage(pmhd_mesh* m, int stage, double dt, double* dt_next, pmhd_sta
 
 int pmhd_gpu_vl2_step(pmhd_mesh* m, double dt, double* dt_next, pmhd_status* st) {
   if (!m) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   if (!m->all_local) return fail(m->ctx, PMHD_ERR_INPUT, "step needs all neighbours local");
   int rc = reset_red(m);
   if (!rc) rc = enqueue_stage(m, 1, dt, true, true);  // + stage-2 interior tiles over the exchange
@@ -894,6 +956,7 @@ int graph_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int
 int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int* cycles_done,
                  pmhd_status* st) {
   if (!m || !t || !dt) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   int rc = PMHD_OK;
   if (!(*dt > 0.0)) {
     rc = pmhd_gpu_new_dt(m, dt, st);
@@ -906,7 +969,9 @@ int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, 
     double h = *dt;
     bool last = false;
     if (tlim > 0.0 && *t + h >= tlim) { h = tlim - *t; last = true; }
-    pmhd_status s;
+    pmhd_status s{};
+    s.code = PMHD_OK;
+    s.k = s.j = s.i = -1;
     double dn = 0.0;
     rc = pmhd_gpu_vl2_step(m, h, &dn, &s);
     floors += s.floor_count;
@@ -927,8 +992,10 @@ int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, 
 
 int pmhd_gpu_diag(pmhd_mesh* m, int kind, double* out) {
   if (!m || !out) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
   const KGeom& G = m->G;
+  if (int rc = drop_prefetch(m)) return rc;
   if (kind == PMHD_DIAG_DIVB_MAX) {
     int rc = reset_red(m);
     if (rc) return rc;
@@ -1001,6 +1068,7 @@ HaloSlab make_slab(const KGeom& G, int dir, int side, bool send) {
 
 int pmhd_gpu_stage_compute(pmhd_mesh* m, int stage, double dt, double* dt_next, pmhd_status* st) {
   if (!m) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   if (stage != 1 && stage != 2) return fail(m->ctx, PMHD_ERR_INPUT, "stage must be 1 or 2");
   if (m->async_ops) {  // reductions of both stages are checked after stage 2
     int rc = (stage == 1) ? reset_red(m) : PMHD_OK;
@@ -1022,6 +1090,7 @@ int pmhd_gpu_stage_compute(pmhd_mesh* m, int stage, double dt, double* dt_next, 
 
 int pmhd_gpu_stage_prefetch(pmhd_mesh* m, int stage, double dt) {
   if (!m) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   if (stage != 2) return fail(m->ctx, PMHD_ERR_INPUT, "only stage 2 can be prefetched");
   if (!can_prefetch(m)) return PMHD_OK;  // stage_compute then runs every tile
   pmhd_ctx* ctx = m->ctx;
@@ -1033,8 +1102,10 @@ int pmhd_gpu_drive_begin(pmhd_mesh* m, int nmode, const int* k, const double* c,
                          const double* const* cos_tab, const double* const* sin_tab, double* sums) {
   if (!m || nmode < 0 || nmode > 64 || (nmode > 0 && (!k || !c || !s)) || !cos_tab || !sin_tab || !sums)
     return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
   const KGeom& G = m->G;
+  if (int rc = drop_prefetch(m)) return rc;
   if (!m->drive_tab) {
     const size_t tab = 2 * 5 * size_t(G.nx[0] + G.nx[1] + G.nx[2]);
     const size_t rows = size_t(G.nb) * (G.ke - G.ks) * ((G.je - G.js) + 1) * 4;  // rows + planes
@@ -1073,7 +1144,9 @@ int pmhd_gpu_drive_begin(pmhd_mesh* m, int nmode, const int* k, const double* c,
 
 int pmhd_gpu_drive_energy(pmhd_mesh* m, const double* mean, double* sums) {
   if (!m || !mean || !sums || !m->drive_tab) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
+  if (int rc = drop_prefetch(m)) return rc;
   launch_drive_sums(m->dblk, m->G, 1, mean, m->drive_rows, m->drive_sums, ctx->stream);
   m->times.kernel_launches += 3;
   CK(cudaGetLastError());
@@ -1085,7 +1158,9 @@ int pmhd_gpu_drive_energy(pmhd_mesh* m, const double* mean, double* sums) {
 
 int pmhd_gpu_drive_apply(pmhd_mesh* m, const double* mean, double scale) {
   if (!m || !mean || !m->drive_tab) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
+  if (int rc = drop_prefetch(m)) return rc;
   launch_drive_apply(m->dblk, m->G, mean, scale, ctx->stream);
   launch_exchange(m->dblk, m->G, 0, ctx->stream);
   m->times.kernel_launches += 1 + m->G.dim;
@@ -1096,6 +1171,7 @@ int pmhd_gpu_drive_apply(pmhd_mesh* m, const double* mean, double scale) {
 
 int pmhd_gpu_slab(const pmhd_mesh* m, void** base, void* ipc_handle) {
   if (!m || !base) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   *base = m->slab;
   if (ipc_handle) {
     cudaIpcMemHandle_t h;
@@ -1117,12 +1193,14 @@ int pmhd_gpu_ipc_open(pmhd_ctx* ctx, const void* ipc_handle, void** base) {
 
 int pmhd_gpu_ipc_close(pmhd_ctx* ctx, void* base) {
   if (!ctx || !base) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(ctx)) return rc_;
   CK(cudaIpcCloseMemHandle(base));
   return PMHD_OK;
 }
 
 int pmhd_gpu_peer_attach(pmhd_mesh* m, int nranks, const int* owner_of_gid, void* const* rank_base) {
   if (!m || nranks < 1 || !owner_of_gid || !rank_base) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
   const KGeom& G = m->G;
   const pmhd_mesh_desc& d = m->desc;
@@ -1168,6 +1246,7 @@ int pmhd_gpu_set_async(pmhd_mesh* m, int on) {
 
 int pmhd_gpu_exchange_dir(pmhd_mesh* m, int dir, int half) {
   if (!m || dir < 0 || dir >= m->G.dim) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
   launch_exchange_dir(m->dblk, m->G, half ? 1 : 0, dir, ctx->stream);
   m->times.kernel_launches += 1;
@@ -1184,6 +1263,7 @@ int pmhd_gpu_halo_count(const pmhd_mesh* m, int dir, int side, long long* n) {
 
 static int halo_xfer(pmhd_mesh* m, int gid, int dir, int side, int half, double* dev_buf, bool pack) {
   if (!m || !dev_buf || dir < 0 || dir >= m->G.dim || side < 0 || side > 1) return PMHD_ERR_INPUT;
+  if (int rc_ = use_device(m->ctx)) return rc_;
   pmhd_ctx* ctx = m->ctx;
   const int b = local_index(m, gid);
   if (b < 0) return fail(ctx, PMHD_ERR_INPUT, "block not local");

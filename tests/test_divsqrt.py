@@ -5,6 +5,9 @@ sqrt(0).
 
 * product variant (PMHD_DIVSQRT_1ULP, the Makefile's FASTDS): MUFU seed + one
   cubic Newton step, no rounding correction -- every result within 1 ulp;
+  its reciprocal square root drsqrt (HLLD's |Bx| / sqrt(rho*)) within 2 ulp
+  of the IEEE expression it replaces, 1 / sqrt(x) (which rounds twice and is
+  itself up to 1 ulp from the exact root; drsqrt rounds once);
 * PMHD_FAST_DIVSQRT alone: the IEEE fast-path sequence -- bit for bit."""
 import ctypes as C
 
@@ -32,7 +35,7 @@ def _run(name):
     a[n // 4: n // 4 + 1000] = np.arange(1000, dtype=np.float64) ** 2
     b[n // 4: n // 4 + 1000] = 2.0 ** rng.integers(-60, 60, 1000)
     a[n // 4] = 0.0
-    out = np.zeros(4, dtype=np.uint64)
+    out = np.zeros(6, dtype=np.uint64)
     rc = L.pmhd_test_divsqrt(a.ctypes.data, b.ctypes.data, n, out.ctypes.data)
     assert rc == 0
     return out
@@ -42,10 +45,14 @@ def test_product_divsqrt_within_one_ulp(gpu_available):
     out = _run("libpmhd_divsqrt_check.so")
     assert out[2] <= 1, f"division off by {out[2]} ulp"
     assert out[3] <= 1, f"sqrt off by {out[3]} ulp"
-    print(f"product variant: {out[0]} divisions and {out[1]} square roots differ from IEEE, by <= 1 ulp")
+    assert out[5] <= 2, f"rsqrt off by {out[5]} ulp from 1/sqrt(x)"
+    assert out[4] > 0 or out[5] == 0
+    print(f"product variant: {out[0]} divisions, {out[1]} square roots and {out[4]} reciprocal roots "
+          "differ from IEEE (max {out[2]}, {out[3]}, {out[5]} ulp)")
 
 
 def test_exact_divsqrt_bitwise_ieee(gpu_available):
     out = _run("libpmhd_divsqrt_exact_check.so")
     assert out[0] == 0, f"{out[0]} divisions differ from IEEE"
     assert out[1] == 0, f"{out[1]} square roots differ from IEEE"
+    assert out[4] == 0 and out[5] == 0  # no drsqrt in this build

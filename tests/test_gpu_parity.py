@@ -183,6 +183,36 @@ def test_config_errors(gpu_available):
     # indexing) -- rejected before any device allocation
     with pytest.raises(ConfigError, match="too large"):
         GpuSolver(RunConfig(nx1=1300, nx2=1300, nx3=1300, mb1=1300, mb2=1300, mb3=1300))
+    # launch-grid limit: every kernel folds the block index into gridDim.z
+    # (<= 65535) with up to n+1 planes of a block; 256^3 in 16^3 blocks is
+    # 4096 blocks x 21 -- rejected up front, not at the first launch
+    with pytest.raises(ConfigError, match="too many MeshBlocks"):
+        GpuSolver(RunConfig(nx1=256, nx2=256, nx3=256, mb1=16, mb2=16, mb3=16))
+
+
+def test_upload_drops_pending_prefetch(gpu_available, monkeypatch):
+    """A stage-2 prefetch (interior flux tiles on the second stream) that is
+    followed by an upload instead of its stage: the upload waits for it and
+    voids it, so the next cycle recomputes every tile and stays bit-identical
+    to the oracle."""
+    monkeypatch.setenv("PMHD_OVERLAP", "1")
+    kw, _ = CASES["wave3d_4blk"]
+    cfg = RunConfig(**kw)
+    o = OracleSolver(cfg, workers=8)
+    g = GpuSolver(cfg, parity=True)
+    o.load_pgen()
+    g.load_pgen()
+    dt = o.new_dt()
+    assert g.new_dt() == dt
+    g.stage_compute(1, dt)
+    g.stage_prefetch(2, dt)
+    for gid in range(cfg.nblocks):  # overwrite the state: the prefetched fluxes are stale
+        g.set_block(gid, o.get_block(gid))
+    g.exchange()
+    o.vl2_step(dt)
+    g.vl2_step(dt)
+    for gid in range(cfg.nblocks):
+        assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
 
 
 def test_unphysical_error_matches_oracle(gpu_available):
