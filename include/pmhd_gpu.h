@@ -243,8 +243,13 @@ int pmhd_gpu_drive_apply(pmhd_mesh* mesh, const double* mean, double scale);
 int pmhd_gpu_diag(pmhd_mesh* mesh, int kind, double* out);
 
 /* Region profiling (with_region, profiler.hpp:90-103; SPEC.md:527 names).
- * When on, every stage records CUDA events between its phases and
- * synchronizes at its end; off (default) adds no synchronization. */
+ * on = 1: every stage records CUDA events between its kernel groups,
+ * launches the instrumented kernel instantiations (clock64 phase shares split
+ * the fused kernels' times into the SPEC regions) and synchronizes at its
+ * end.  on = 2: the same events around the product kernels, without the
+ * phase instrumentation: riemann_ms then holds the whole flux-kernel time
+ * and integrate_ms the whole update-kernel time (c2p / reconstruct / ct_emf
+ * stay 0 for the fused kernels).  0 (default) adds no synchronization. */
 int pmhd_gpu_set_profiling(pmhd_mesh* mesh, int on);
 /* Accumulated region times (out may be NULL); reset != 0 zeroes them. */
 int pmhd_gpu_region_times(pmhd_mesh* mesh, pmhd_region_times* out, int reset);

@@ -139,7 +139,7 @@ void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir,
 // kd: nullptr (coefficients by value) or the device copy of a graph-replayed cycle
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
                        int plm, double c1024, const KStage* kd, int stage, DevRed* red, int slab,
-                       int nslab, int S, cudaStream_t s, int region = 0);
+                       int nslab, int S, cudaStream_t s, int region = 0, int reuse = 0);
 void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s);
 // ec_maps (optional, 3D meshes): per block, TMA tensor maps of its 3 cell-E
 // arrays (box = the update tile's E box) -- the kernel then streams its E

@@ -90,13 +90,76 @@ __device__ __forceinline__ int rot_var(int n) {
   return V[DIR][n];
 }
 
+// Owned-face reuse (launch flag `reuse`; every neighbour of every block on
+// this rank, diagonals included, is local and the blocks form a regular
+// periodic grid).  The update kernel reads face data on the block's halo
+// positions too: the upper normal face e of each direction and the
+// transverse faces at s-1 and e.  Each of those equals, bit for bit, a face
+// some block computes inside its own range [s, e) -- the ghost cells are
+// exact copies, so the stencils are the same values -- so tiles cover only
+// [s, e) on every axis and a face on the rim of that range is also stored
+// at the halo positions that image it: coordinate s -> the lower neighbour's
+// e (shift +mb), coordinate e-1 -> the upper neighbour's s-1 (shift -mb; not
+// along the face's own normal axis, which has no s-1 face), and every
+// combination of those across axes (edge and corner images).  The same for
+// the cell-centred E the last direction writes (cells s-1 and e of the two
+// tile axes in the plane).  At 256^3 this removes the partial tiles of the
+// extended ranges (x1: 257 faces in 9 tiles of 32, x2/x3: 258 in 17 of 16),
+// 12-15 % of the flux CTAs; with 64^3 blocks about a third.
+// axes: bit a set = axis a may image; normal: the axis that images its s
+// only (-1: none).  ci/cj/ck: the value's coordinates.  SEL 0..2: the face
+// data of that direction (vals in rotated order, stored to the lab-order
+// arrays); SEL 3: the cell-centred E (3 values).  Fully unrolled, so the
+// bookkeeping stays in registers.
+template <int SEL>
+__device__ __forceinline__ void rim_images(const DevBlock* __restrict__ blks, int b, const KGeom& G, int axes,
+                                           int normal, int ci, int cj, int ck, int id, const double* vals) {
+  constexpr int NV = (SEL < 3) ? 8 : 3;
+  const int c[3] = {ci, cj, ck}, s[3] = {G.is, G.js, G.ks}, e[3] = {G.ie, G.je, G.ke};
+  const int st[3] = {1, G.sx, G.sy};
+  int side[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    side[a] = -1;
+    if ((axes >> a) & 1) {
+      if (c[a] == s[a]) side[a] = 0;
+      else if (c[a] == e[a] - 1 && a != normal) side[a] = 1;
+    }
+  }
+  if (side[0] < 0 && side[1] < 0 && side[2] < 0) return;
+#pragma unroll
+  for (int msk = 1; msk < 8; ++msk) {
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (((msk >> a) & 1) && side[a] < 0) ok = false;
+    if (!ok) continue;
+    int t = b, off = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if ((msk >> a) & 1) {
+        t = blks[t].nbr[a][side[a]];
+        off += (side[a] == 0 ? G.mb[a] : -G.mb[a]) * st[a];
+      }
+    const DevBlock& TB = blks[t];
+    PMHD_CHECK_ID(G, id + off);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double* dst;
+      if constexpr (SEL < 3) dst = TB.fx[SEL][(v >= 1 && v <= 3) ? rot_var<SEL>(v) : v];
+      else dst = TB.ec[v];
+      __stcs(dst + id + off, vals[v]);
+    }
+  }
+}
+
 // MODE: 0 product, 1 region profiling (phase clocks), 2 graph-replayed cycle
 // (coefficient and skip flag read from the device copy kd)
 template <int DIR, int RS, int MODE>
 __global__ void __launch_bounds__(NTHR, FluxMinB<RS>::value)
 k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024_arg,
              const KStage* __restrict__ kd, int stage, DevRed* red, int write_ec, int f_i0, int f_i1,
-             int f_s0, int f_s1, int f_t0, int f_t1, int ty0, int region) {
+             int f_s0, int f_s1, int f_t0, int f_t1, int ty0, int region, int reuse) {
   constexpr bool PROF = (MODE == 1);
   if (MODE == 2 && kd->skip) return;  // replayed cycle past the end of the run: no loads either
   using TS = TileShape<DIR>;
@@ -160,11 +223,18 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       // cells of this tile's own face rows [fs0, fs0+8) clipped to the face
       // range, plus the row below the block's first face row
       const int s = (DIR == 2) ? k : j;
-      const bool own = (s >= fs0 && s < fs0 + FS && s < f_s1) || (fs0 == f_s0 && s == f_s0 - 1);
+      // (owned face ranges: also the row above the last face row, which the
+      // extended ranges covered as a face row of their own)
+      const bool own = (s >= fs0 && s < fs0 + FS && s < f_s1) || (fs0 == f_s0 && s == f_s0 - 1) ||
+                       (reuse && s == f_s1 && fs0 + FS >= f_s1);
       if (own && i >= f_i0 && i < f_i1) {
-        B.ec[0][id] = w[3] * w[6] - w[2] * w[7];
-        B.ec[1][id] = w[1] * w[7] - w[3] * w[5];
-        B.ec[2][id] = w[2] * w[5] - w[1] * w[6];
+        const double ev[3] = {w[3] * w[6] - w[2] * w[7], w[1] * w[7] - w[3] * w[5], w[2] * w[5] - w[1] * w[6]};
+        B.ec[0][id] = ev[0];
+        B.ec[1][id] = ev[1];
+        B.ec[2][id] = ev[2];
+        if (reuse) {  // images on the neighbours' halo columns / rows of the plane
+          rim_images<3>(blks, b, G, (DIR == 2) ? 3 : 1, -1, i, j, k, id, ev);
+        }
       }
     }
 #pragma unroll
@@ -338,6 +408,9 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     F[6][id] = out[6];
     F[7][id] = out[7];
 #endif
+    if (reuse) {  // a face on the rim of the owned range: its halo images
+      rim_images<DIR>(blks, b, G, (G.dim == 3) ? 7 : 3, DIR, i, j, k, id, out);
+    }
   }
   if (PROF) {
     __syncthreads();
@@ -358,11 +431,13 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 // multiple of the x3 tile's FS (16).  nslab = 1 is the whole block.
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
                        int plm, double c1024, const KStage* kd, int stage, DevRed* red, int slab,
-                       int nslab, int S, cudaStream_t s, int region) {
+                       int nslab, int S, cudaStream_t s, int region, int reuse) {
   const int d3 = (G.dim == 3) ? 1 : 0;
-  // face ranges of the oracle: [lo, hi) per axis
+  // face ranges of the oracle: [lo, hi) per axis;
+  // with owned-face reuse [s, e) on every axis (the rest are rim images)
   int i0, i1, j0, j1, k0, k1;
-  if (dir == 0) { k0 = G.ks - d3; k1 = G.ke + d3; j0 = G.js - 1; j1 = G.je + 1; i0 = G.is; i1 = G.ie + 1; }
+  if (reuse) { k0 = G.ks; k1 = G.ke; j0 = G.js; j1 = G.je; i0 = G.is; i1 = G.ie; }
+  else if (dir == 0) { k0 = G.ks - d3; k1 = G.ke + d3; j0 = G.js - 1; j1 = G.je + 1; i0 = G.is; i1 = G.ie + 1; }
   else if (dir == 1) { k0 = G.ks - d3; k1 = G.ke + d3; j0 = G.js; j1 = G.je + 1; i0 = G.is - 1; i1 = G.ie + 1; }
   else { k0 = G.ks; k1 = G.ke + 1; j0 = G.js - 1; j1 = G.je + 1; i0 = G.is - 1; i1 = G.ie + 1; }
   const int ns0 = (dir == 2) ? k0 : j0, ns1 = (dir == 2) ? k1 : j1;
@@ -388,13 +463,13 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   do {                                                                                              \
     if (kd)                                                                                         \
       k_flux_fused<D, R, 2><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
-                                                  write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
+                                                  write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region, reuse); \
     else if (ph.prof)                                                                               \
       k_flux_fused<D, R, 1><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
-                                                  write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
+                                                  write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region, reuse); \
     else                                                                                            \
       k_flux_fused<D, R, 0><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
-                                                  write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region); \
+                                                  write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region, reuse); \
   } while (0)
 #define PMHD_FLUX_DIRS(R)                          \
   do {                                             \

@@ -91,6 +91,7 @@ struct pmhd_mesh {
   int variant = 0;                // 0: fused flux kernels; 1: split (debug; PMHD_KERNELS=split)
   int slab_planes = 0;            // k-slab pipeline depth (PMHD_SLAB_PLANES, 0 = off)
   bool push_x1 = false;           // update kernel writes the x1 ghosts (PMHD_PUSH_X1, default on when possible)
+  bool face_reuse = false;        // flux tiles cover owned faces only + rim images (PMHD_FACE_REUSE)
   std::vector<cudaEvent_t> slab_ev;
   cudaEvent_t ev[8] = {};
   cudaEvent_t xev[25] = {};        // host<->device transfer pipeline (one per staged array + 1)
@@ -247,7 +248,7 @@ int prefetch_stage(pmhd_mesh* m, int s, double dt) {
   CK(cudaStreamWaitEvent(ctx->stream2, m->ev_pre[0], 0));
   for (int dir = 0; dir < G.dim; ++dir)
     launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], nullptr, s, m->dred, 0,
-                      1, G.ke - G.ks, ctx->stream2, 1);
+                      1, G.ke - G.ks, ctx->stream2, 1, m->face_reuse ? 1 : 0);
   CK(cudaEventRecord(m->ev_pre[1], ctx->stream2));
   m->times.kernel_launches += G.dim;
   m->prefetched = s;
@@ -313,7 +314,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     for (int dir = 0; dir < G.dim; ++dir) {
       if (m->variant == 0)
         launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], kd, s, m->dred, 0, 1,
-                          nk, st, flux_region);
+                          nk, st, flux_region, m->face_reuse ? 1 : 0);
       else
         launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], st);
     }
@@ -660,6 +661,11 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   }
   if (G.mb[0] < G.ng) m->push_x1 = false;
   if (const char* px = std::getenv("PMHD_PUSH_X1")) m->push_x1 = m->push_x1 && std::atoi(px) != 0;
+  // owned-face reuse (kernels_flux.cu): every neighbour local, so every
+  // halo face the update reads has an owner on this rank; not with the
+  // k-slab pipeline (images cross slabs)
+  m->face_reuse = m->all_local && m->slab_planes == 0;
+  if (const char* fr = std::getenv("PMHD_FACE_REUSE")) m->face_reuse = m->face_reuse && std::atoi(fr) != 0;
   m->slab_ev.resize((G.ke - G.ks) / 8 + 2);
   for (auto& e : m->slab_ev) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   MCK(cudaStreamSynchronize(ctx->stream));
@@ -1286,8 +1292,9 @@ int pmhd_gpu_halo_unpack(pmhd_mesh* m, int gid, int dir, int side, int half, con
 
 int pmhd_gpu_set_profiling(pmhd_mesh* m, int on) {
   if (!m) return PMHD_ERR_INPUT;
+  if (on < 0 || on > 2) return fail(m->ctx, PMHD_ERR_INPUT, "profiling mode must be 0, 1 or 2");
   m->prof = on != 0;
-  m->ph.prof = m->prof ? 1 : 0;
+  m->ph.prof = (on == 1) ? 1 : 0;  // 2: events only, product kernels
   return PMHD_OK;
 }
 

@@ -257,6 +257,32 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
         assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
 
 
+@pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_ragged", "wave3d_tiny_blocks",
+                                  "wave3d_ng3_ragged", "turb3d"])
+def test_face_reuse_bitwise(gpu_available, case, monkeypatch):
+    """Owned-face reuse (flux tiles over [s, e) only, halo faces and cell E
+    stored as rim images by their owners) leaves the product (FMA) build's
+    results unchanged bit for bit: the images are the values the extended
+    face ranges computed from the exact ghost copies."""
+    kw, ncyc = CASES[case]
+    cfg = RunConfig(**kw)
+    out = []
+    for reuse in ("0", "1"):
+        monkeypatch.setenv("PMHD_FACE_REUSE", reuse)
+        g = GpuSolver(cfg)
+        g.load_pgen()
+        dt = g.new_dt()
+        dts = []
+        for _ in range(ncyc):
+            dt, _st = g.vl2_step(dt)
+            dts.append(dt)
+        out.append((dts, [g.get_block(gid) for gid in range(cfg.nblocks)]))
+    assert out[0][0] == out[1][0]
+    for b0, b1 in zip(out[0][1], out[1][1]):
+        for f in ("u", "b1f", "b2f", "b3f"):
+            assert np.array_equal(getattr(b0, f), getattr(b1, f)), (case, f)
+
+
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_4blk"])
 def test_overlap_prefetch_bitwise(gpu_available, case, monkeypatch):
     """Stage-2 interior flux tiles enqueued on a second stream while the

@@ -13,6 +13,11 @@ for v in "$@"; do
     slab*) PMHD_SLAB_PLANES=${v#slab} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     notma) PMHD_TMA=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     nooverlap) PMHD_OVERLAP=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    noreuse) PMHD_FACE_REUSE=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5) $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5noreuse) PMHD_FACE_REUSE=0 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    b128) $B --block 128 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    b128noreuse) PMHD_FACE_REUSE=0 $B --block 128 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     hlle|roe) $B --riemann $v > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     *-hlle|*-roe) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_${v%-*}.so $B --riemann ${v##*-} > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     parity) PMHD_GPU_LIB=paper_1905_04341_b200/lib/libpmhd_gpu_parity.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
