@@ -148,6 +148,16 @@ void launch_update_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, 
                          const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s,
                          const CUtensorMap* ec_maps = nullptr, int push = 0);
 void update_ec_box(int box[2]);
+// TMA-staged update kernel (kernels_update_tma.cu, 3D meshes): maps[b * per
+// block + id] are the tensor maps of block b for the table the launch uses;
+// bit id of xoffm = 1 when that map starts one element before its array (16 B
+// alignment of the map base).
+int update_tma_maps_per_block();
+void update_tma_box(int id, int box[3]);  // width, height, first cell rel. to the tile origin
+const double* update_tma_array(const DevBlock& B, int id);
+void launch_update_tma(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
+                       const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s,
+                       const CUtensorMap* maps, unsigned long long xoffm, int push);
 bool update_uses_tma();  // built with PMHD_UPDATE_TMA
 void launch_update(const DevBlock* blks, const KGeom& G, const KStage& ks, cudaStream_t s);
 void launch_c2p_end(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,

@@ -16,6 +16,7 @@
 #include <atomic>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace pmhd_gpu {
 
@@ -55,34 +56,6 @@ __device__ __forceinline__ void ST(double* p, double v) {
 #else
   *p = v;
 #endif
-}
-
-// ---- TMA + mbarrier (PTX) ----------------------------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, unsigned long long* bar, int x,
-                                            int y, int z) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-      : "memory");
 }
 
 // Shared memory of one CTA (dynamic: > 48 KB for 32 x 16 tiles).
@@ -241,7 +214,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
   auto issue_ec = [&](int kk) {
     if (tid == 0) {
       const int sl = kk & 1;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads of the slot
+      fence_proxy_async_smem();  // after the generic reads of the slot
       mbar_expect_tx(&SM.bar[sl], 3u * EX * EY * 8u);
       for (int c = 0; c < 3; ++c)  // the maps start at i = -1: cell i0-1 is x = i0
         tma_load_3d(&SM.ecbuf[c][sl][0], ec_maps + 3 * b + c, &SM.bar[sl], i0, j0 - 1, kk);
@@ -258,7 +231,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
     if (tid == 0) {
       mbar_init(&SM.bar[0], 1);
       mbar_init(&SM.bar[1], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_init_fence();
     }
     __syncthreads();
     issue_ec(kb - 1);

@@ -74,6 +74,10 @@ struct pmhd_mesh {
   // device copies of the stage coefficients (dks[1], dks[2]) and the run
   // control of a graph-replayed pmhd_gpu_run; graphs cached per table parity
   CUtensorMap* ec_maps = nullptr;  // TMA maps of the cell-E arrays (3 per block; nullptr: plain loads)
+  // TMA-staged update kernel (3D, PMHD_UPDATE=tma): per table parity, per
+  // block, the maps of kernels_update_tma.cu; nullptr = the LDG update kernel
+  CUtensorMap* upd_maps = nullptr;
+  unsigned long long upd_xoff = 0;
   KStage* dks = nullptr;
   DevCtl* dctl = nullptr;
   int parity = 0;                 // table flips mod 2 (hblk/dblk vs their alternates)
@@ -219,6 +223,72 @@ int build_ec_maps(pmhd_mesh* m) {
   return PMHD_OK;
 }
 
+// Tensor maps of the TMA-staged update kernel, for both block tables (the
+// tables swap u^n and u^{n+1} every cycle): 3D over each pitched array,
+// dims (n1+1 [+1], n2+1, n3+1), one box shape per map id.  A map whose
+// array is not 16 B aligned starts one element early (bit set in upd_xoff).
+// Box starts must be 16 B aligned too: if the row alignment does not give
+// that (PMHD_ROW_SHIFT* overrides), no maps are built and the LDG update
+// kernel runs.
+int build_update_maps(pmhd_mesh* m) {
+  const KGeom& G = m->G;
+  if (G.dim != 3) return PMHD_OK;
+  // opt-in (PMHD_UPDATE=tma): measured slower than the LDG kernel at 256^3
+  // (1.64 vs 1.55 ms per launch)
+  const char* u = std::getenv("PMHD_UPDATE");
+  if (!u || std::string(u) != "tma") return PMHD_OK;
+  pmhd_ctx* ctx = m->ctx;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return PMHD_OK;  // no driver entry point: the LDG update kernel
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  const int per = update_tma_maps_per_block();
+  std::vector<CUtensorMap> maps(size_t(2) * G.nb * per);
+  unsigned long long xoff = 0;
+  for (int par = 0; par < 2; ++par)
+    for (int b = 0; b < G.nb; ++b)
+      for (int a = 0; a < per; ++a) {
+        const DevBlock& B = (par == 0 ? m->hblk : m->hblk_alt)[b];
+        const double* arr = update_tma_array(B, a);
+        const int xo = int((reinterpret_cast<uintptr_t>(arr) / 8) & 1);
+        if (par == 0 && b == 0) xoff |= (unsigned long long)xo << a;
+        else if (((xoff >> a) & 1ull) != (unsigned long long)xo) return PMHD_OK;  // (never: uniform shifts)
+        int box[3];
+        update_tma_box(a, box);
+        // every box starts on a 16 B boundary: tile origins are is + 32 n, so
+        // the element parity of (is + first cell) must put it there
+        if (((reinterpret_cast<uintptr_t>(arr) / 8) + unsigned(G.is + box[2])) & 1u) return PMHD_OK;
+        const cuuint64_t dim[3] = {cuuint64_t(G.n1 + 1 + xo), cuuint64_t(G.n2 + 1), cuuint64_t(G.n3 + 1)};
+        const cuuint64_t stride[2] = {cuuint64_t(G.sx) * 8, cuuint64_t(G.sy) * 8};
+        const cuuint32_t bx[3] = {cuuint32_t(box[0]), cuuint32_t(box[1]), 1};
+        const cuuint32_t es[3] = {1, 1, 1};
+        const CUresult r = encode(&maps[(size_t(par) * G.nb + b) * per + a], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                                  const_cast<double*>(arr - xo), dim, stride, bx, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(ctx, PMHD_ERR_CUDA, "cuTensorMapEncodeTiled (update maps) failed");
+      }
+  CK(cudaMalloc(&m->upd_maps, maps.size() * sizeof(CUtensorMap)));
+  CK(cudaMemcpy(m->upd_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  m->upd_xoff = xoff;
+  return PMHD_OK;
+}
+
+// The fused update kernel of one stage over planes [kr0, kr1): the
+// TMA-staged kernel when its maps exist (3D, PMHD_UPDATE=tma), else the LDG
+// kernel (default).
+void launch_update_any(pmhd_mesh* m, const KStage& ks, const KStage* kd, int want_dt, int kr0, int kr1,
+                       cudaStream_t st, int push) {
+  if (m->upd_maps) {
+    const CUtensorMap* maps = m->upd_maps + size_t(m->parity) * m->G.nb * update_tma_maps_per_block();
+    launch_update_tma(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, maps, m->upd_xoff, push);
+  } else {
+    launch_update_fused(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, m->ec_maps, push);
+  }
+}
+
 KStage make_stage(const KGeom& G, int s, double dt) {
   const double beta = (s == 1) ? 0.5 : 1.0;
   const double bdt = beta * dt;
@@ -296,13 +366,11 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
       CK(cudaEventRecord(m->slab_ev[q], st));
       if (q >= 1) {  // update slab q-1 once the flux kernels of slab q are done
         CK(cudaStreamWaitEvent(ctx->stream2, m->slab_ev[q], 0));
-        launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks + (q - 1) * S,
-                            G.ks + q * S, ctx->stream2, m->ec_maps);
+        launch_update_any(m, ks, kd, s == 2, G.ks + (q - 1) * S, G.ks + q * S, ctx->stream2, 0);
       }
     }
     CK(cudaStreamWaitEvent(ctx->stream2, m->slab_ev[nslab - 1], 0));
-    launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks + (nslab - 1) * S, G.ke,
-                        ctx->stream2, m->ec_maps);
+    launch_update_any(m, ks, kd, s == 2, G.ks + (nslab - 1) * S, G.ke, ctx->stream2, 0);
     CK(cudaEventRecord(m->slab_ev[nslab], ctx->stream2));
     CK(cudaStreamWaitEvent(st, m->slab_ev[nslab], 0));
     if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st, kd);
@@ -322,8 +390,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     if (m->variant == 1) launch_emf(m->dblk, G, m->ph, st);
     rec(m, 3);
     if (m->variant == 0) {
-      launch_update_fused(m->dblk, G, m->ph, ks, kd, m->dred, s == 2, G.ks, G.ke, st, m->ec_maps,
-                          m->push_x1 ? 1 : 0);
+      launch_update_any(m, ks, kd, s == 2, G.ks, G.ke, st, m->push_x1 ? 1 : 0);
     } else {
       launch_update(m->dblk, G, ks, st);
       launch_c2p_end(m->dblk, G, m->ph, ks, m->dred, s == 2, st);
@@ -635,6 +702,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   MCK(cudaMalloc(&m->dks, 3 * sizeof(KStage)));
   if (G.dim == 3) {
     int rc = build_ec_maps(m);
+    if (!rc) rc = build_update_maps(m);
     if (rc) { pmhd_gpu_mesh_destroy(m); return rc; }
   }
   MCK(cudaMalloc(&m->dctl, sizeof(DevCtl)));
@@ -684,6 +752,7 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   cudaFree(m->dred);
   cudaFree(m->dks);
   if (m->ec_maps) cudaFree(m->ec_maps);
+  if (m->upd_maps) cudaFree(m->upd_maps);
   cudaFree(m->dctl);
   for (auto& g : m->gexec) if (g) cudaGraphExecDestroy(g);
   cudaFree(m->drows);

@@ -257,6 +257,34 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
         assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
 
 
+@pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "wave3d_tiny_blocks", "wave3d_ng3_ragged",
+                                  "wave3d_ng4_8blk", "turb3d", "blast3d_64_floor"])
+def test_update_kernels_bitwise(gpu_available, case, monkeypatch):
+    """The TMA-staged update kernel (3D, PMHD_UPDATE=tma) and the default LDG
+    update kernel compute the same expressions on the same operands: the
+    parity build gives the same bits with either (the FMA build may contract
+    a multiply-add differently in the two kernels; it is held to the oracle
+    tolerance by test_fma_build_within_tolerance)."""
+    kw, ncyc = CASES[case]
+    cfg = RunConfig(**kw)
+    out = []
+    for kern in ("ldg", "tma"):
+        monkeypatch.setenv("PMHD_UPDATE", kern)
+        g = GpuSolver(cfg, parity=True)
+        g.load_pgen()
+        dt = g.new_dt()
+        dts, floors = [], 0
+        for _ in range(ncyc):
+            dt, st = g.vl2_step(dt)
+            dts.append(dt)
+            floors += st.floor_count
+        out.append((dts, floors, [g.get_block(gid) for gid in range(cfg.nblocks)]))
+    assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
+    for b0, b1 in zip(out[0][2], out[1][2]):
+        for f in ("u", "b1f", "b2f", "b3f"):
+            assert np.array_equal(getattr(b0, f), getattr(b1, f)), (case, f)
+
+
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_ragged", "wave3d_tiny_blocks",
                                   "wave3d_ng3_ragged", "turb3d"])
 def test_face_reuse_bitwise(gpu_available, case, monkeypatch):

@@ -1,8 +1,8 @@
 #!/bin/bash
 # A/B bench session: parity tests, then short benches of variants.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -4 gpurun_out/pytest_gpu.log
+[ -z "$NO_PYTEST" ] && { timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log; }
+[ -z "$NO_PYTEST" ] && tail -4 gpurun_out/pytest_gpu.log
 B="python bench.py --steps 6 --warmup 3 --no-cpu-baseline --no-e2e"
 for v in "$@"; do
   case $v in
@@ -13,6 +13,8 @@ for v in "$@"; do
     slab*) PMHD_SLAB_PLANES=${v#slab} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     notma) PMHD_TMA=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     nooverlap) PMHD_OVERLAP=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    tma) PMHD_UPDATE=tma $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5tma) PMHD_UPDATE=tma $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     noreuse) PMHD_FACE_REUSE=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5) $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5noreuse) PMHD_FACE_REUSE=0 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
