@@ -18,6 +18,8 @@
 // The last direction's kernel also writes the cell-centred E = -v x B of the
 // box the fused update kernel needs (cells [is-1,ie] x [js-1,je] x [ks-1,ke]),
 // so that kernel does not redo cons_to_prim.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace pmhd_gpu {
@@ -423,6 +425,190 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   }
 }
 
+//---------------------------------------------------------------------------
+// Column-march flux kernel for the x2 and x3 faces (DIR 1: march along j,
+// DIR 2: march along k).  Their stencil runs along an axis the threads of a
+// warp do not share (a warp is 32 consecutive i), so each thread owns one
+// face column and walks it: per step it loads and converts ONE new cell,
+// forms ONE PLM slope and solves ONE face, keeping the last three cells'
+// rotated primitives and the reconstructed side states in a private slice of
+// shared memory ([var][thread], conflict-free; HLLD reads its side states
+// from there through SmemW as in k_flux_fused).  No thread reads another
+// thread's data, so there is no __syncthreads at all, and a column segment
+// of L faces converts L + 3 cells (the tile kernel: 1.19 per face).  Same
+// expressions and operand order as k_flux_fused, so the same bits.
+#ifndef PMHD_MARCH_L
+#define PMHD_MARCH_L 32  // faces per column segment
+#endif
+constexpr int MT = 128;  // threads: 32 i x 4 transverse columns
+#ifndef PMHD_MARCH_MINB
+#define PMHD_MARCH_MINB 4  // CTAs per SM the registers are sized for (5 spills 24-32 B)
+#endif
+template <int RS>
+struct MarchMinB {
+  static constexpr int value = PMHD_MARCH_MINB ? PMHD_MARCH_MINB : FluxMinB<RS>::value;
+};
+template <int DIR, int RS, int MODE>
+__global__ void __launch_bounds__(MT, MarchMinB<RS>::value)
+k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024_arg,
+             const KStage* __restrict__ kd, int stage, DevRed* red, int write_ec, int f_i0, int f_i1, int f_m0,
+             int f_m1, int f_t0, int f_t1, int region, int reuse) {
+  static_assert(DIR == 1 || DIR == 2, "column march: x2 / x3 faces");
+  constexpr bool PROF = (MODE == 1);
+  if (MODE == 2 && kd->skip) return;
+  // private ring: P[slot][var][thread] primitives of the last 3 cells (rotated
+  // order), WL[2] high-face states of the previous / this cell, WR the
+  // low-face state of this cell (stage 2); stage 1 reads P directly
+  __shared__ double P[3][7][MT];
+  __shared__ double WL[2][7][MT];
+  __shared__ double WR[7][MT];
+  const int nm = (f_m1 - f_m0 + PMHD_MARCH_L - 1) / PMHD_MARCH_L;
+  const int b = blockIdx.z / nm;
+  const int m0 = f_m0 + (int)(blockIdx.z % nm) * PMHD_MARCH_L;
+  const int m1 = min(m0 + PMHD_MARCH_L, f_m1);
+  const int i = f_i0 + blockIdx.x * 32 + (threadIdx.x & 31);
+  const int t = f_t0 + blockIdx.y * 4 + (threadIdx.x >> 5);
+  const DevBlock& B = blks[b];
+  double* const* S = B.st[sel];
+  if (region != 0) {  // as k_flux_fused: region 1 = segments clear of the ghost exchange
+    const int ci0 = f_i0 + blockIdx.x * 32, ct0 = f_t0 + blockIdx.y * 4;
+    int c0[3], c1[3];
+    c0[0] = ci0; c1[0] = ci0 + 31;
+    if (DIR == 1) { c0[1] = m0 - 2; c1[1] = m1 + 1; c0[2] = ct0; c1[2] = ct0 + 3; }
+    else { c0[2] = m0 - 2; c1[2] = m1 + 1; c0[1] = ct0; c1[1] = ct0 + 3; }
+    bool inner = c0[0] >= G.is + 1 && c1[0] <= G.ie - 1 && c0[1] >= G.js + 1 && c1[1] <= G.je - 1;
+    if (G.dim == 3) inner = inner && c0[2] >= G.ks + 1 && c1[2] <= G.ke - 1;
+    if (inner != (region == 1)) return;
+  }
+  if (i >= f_i1 || t >= f_t1) return;  // (no barriers below)
+  const int tid = threadIdx.x;
+  long long tc = 0, tp = 0, tr = 0, tck = 0;  // profiling (thread 0): c2p / PLM / Riemann cycles
+  auto cid = [&](int m) { return (DIR == 2) ? G.idx(m, t, i) : G.idx(t, m, i); };
+  // load + cons_to_prim of the cell at march position m into ring slot sl
+  // (and its cell-centred E where this segment owns it)
+  auto cell = [&](int m, int sl) {
+    const bool in = (m >= 0 && m < ((DIR == 2) ? G.n3 : G.n2));
+    if (!in) return;
+    const int id = cid(m);
+    PMHD_CHECK_ID(G, id + G.sy);
+    double ub[11];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) ub[v] = __ldg(S[v] + id);
+    ub[5] = __ldg(S[5] + id);
+    ub[6] = __ldg(S[5] + id + 1);
+    ub[7] = __ldg(S[6] + id);
+    ub[8] = __ldg(S[6] + id + G.sx);
+    ub[9] = __ldg(S[7] + id);
+    ub[10] = __ldg(S[7] + id + G.sy);
+    double u[5], bc[3], w[8];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = ub[v];
+    bc[0] = 0.5 * (ub[5] + ub[6]);
+    bc[1] = 0.5 * (ub[7] + ub[8]);
+    bc[2] = 0.5 * (ub[9] + ub[10]);
+    const int fl = cons_to_prim(u, bc, ph, w, false);
+    const int k = (DIR == 2) ? m : t, j = (DIR == 2) ? t : m;
+    if ((fl & 4) && k >= G.ks && k < G.ke && j >= G.js && j < G.je && i >= G.is && i < G.ie) {
+      const long long gi = (long long)B.c[0] * G.mb[0] + (i - G.is);
+      const long long gj = (long long)B.c[1] * G.mb[1] + (j - G.js);
+      const long long gk = (G.dim == 3) ? (long long)B.c[2] * G.mb[2] + (k - G.ks) : 0;
+      atomicMin(&red[stage].bad_key, (unsigned long long)((gk * G.nx[1] + gj) * G.nx[0] + gi));
+    }
+    if (write_ec) {
+      // rows [f_m0 - 1, f_m1) (+ f_m1 with owned ranges), each by one segment
+      const bool own = (m >= m0 && m < m1) || (m0 == f_m0 && m == f_m0 - 1) || (reuse && m == f_m1 && m1 == f_m1);
+      if (own) {
+        const double ev[3] = {w[3] * w[6] - w[2] * w[7], w[1] * w[7] - w[3] * w[5], w[2] * w[5] - w[1] * w[6]};
+        B.ec[0][id] = ev[0];
+        B.ec[1][id] = ev[1];
+        B.ec[2][id] = ev[2];
+        if (reuse) rim_images<3>(blks, b, G, (DIR == 2) ? 3 : 1, -1, i, j, k, id, ev);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < 7; ++n) P[sl][n][tid] = w[rot_var<DIR>(n)];
+  };
+  const double c1024 = (MODE == 2) ? kd->c1024[DIR] : c1024_arg;
+  // prologue: cells m0-2, m0-1 (donor: m0-1 is the first face's low side;
+  // PLM: both feed the first slope), ring slot = position mod 3
+  auto slot = [](int m) { return ((m % 3) + 3) % 3; };
+  if (PROF && tid == 0) tck = clock64();
+  cell(m0 - 2, slot(m0 - 2));
+  cell(m0 - 1, slot(m0 - 1));
+  if (plm) {
+    // high-face state of cell m0-1 (slope from m0-2, m0-1, m0)
+    cell(m0, slot(m0));
+#pragma unroll
+    for (int n = 0; n < 7; ++n) {
+      const double q0 = P[slot(m0 - 1)][n][tid];
+      const double dq = plm_slope(P[slot(m0 - 2)][n][tid], q0, P[slot(m0)][n][tid], ph.limiter);
+      WL[(m0 - 1) & 1][n][tid] = q0 + 0.5 * dq;
+    }
+  }
+  if (PROF && tid == 0) { const long long c = clock64(); tc += c - tck; tck = c; }
+  for (int f = m0; f < m1; ++f) {
+    // cell f (donor) / f+1 (PLM) -- the last one the face at f needs
+    if (plm) cell(f + 1, slot(f + 1));
+    else cell(f, slot(f));
+    if (PROF && tid == 0) { const long long c = clock64(); tc += c - tck; tck = c; }
+    const double* wlp;
+    const double* wrp;
+    if (plm) {
+#pragma unroll
+      for (int n = 0; n < 7; ++n) {
+        const double q0 = P[slot(f)][n][tid];
+        const double dq = plm_slope(P[slot(f - 1)][n][tid], q0, P[slot(f + 1)][n][tid], ph.limiter);
+        WL[f & 1][n][tid] = q0 + 0.5 * dq;  // wL of face f+1
+        WR[n][tid] = q0 - 0.5 * dq;         // wR of face f
+      }
+      wlp = &WL[(f - 1) & 1][0][tid];
+      wrp = &WR[0][tid];
+    } else {
+      wlp = &P[slot(f - 1)][0][tid];
+      wrp = &P[slot(f)][0][tid];
+    }
+    if (PROF && tid == 0) { const long long c = clock64(); tp += c - tck; tck = c; }
+    const int k = (DIR == 2) ? f : t, j = (DIR == 2) ? t : f;
+    const int id = cid(f);
+    PMHD_CHECK_ID(G, id);
+    const double bn = __ldg(S[5 + DIR] + id);
+    double out[8];
+    int fb;
+    if constexpr (PMHD_FLUX_SMEMW && (RS == PMHD_RIEMANN_HLLD || RS == PMHD_RIEMANN_ROE)) {
+      const SmemW wl{wlp, MT}, wr{wrp, MT};
+      fb = face_solve<RS>(wl, wr, bn, ph, c1024, out);
+    } else {
+      double wl[7], wr[7];
+#pragma unroll
+      for (int n = 0; n < 7; ++n) {
+        wl[n] = wlp[n * MT];
+        wr[n] = wrp[n * MT];
+      }
+      fb = face_solve<RS>(wl, wr, bn, ph, c1024, out);
+    }
+    if (fb) atomicAdd(&red[stage].fallback_count, 1ULL);
+    double* const* F = B.fx[DIR];
+    __stcs(F[0] + id, out[0]);
+    __stcs(F[rot_var<DIR>(1)] + id, out[1]);
+    __stcs(F[rot_var<DIR>(2)] + id, out[2]);
+    __stcs(F[rot_var<DIR>(3)] + id, out[3]);
+    __stcs(F[4] + id, out[4]);
+    __stcs(F[5] + id, out[5]);
+    __stcs(F[6] + id, out[6]);
+    __stcs(F[7] + id, out[7]);
+    if (reuse) rim_images<DIR>(blks, b, G, (G.dim == 3) ? 7 : 3, DIR, i, j, k, id, out);
+    if (PROF && tid == 0) { const long long c = clock64(); tr += c - tck; tck = c; }
+  }
+  // donor cell with owned ranges: the cell-centred E row f_m1 is no face's
+  // stencil cell here, but the update kernel's E box needs it
+  if (write_ec && reuse && !plm && m1 == f_m1) cell(f_m1, slot(f_m1));
+  if (PROF && tid == 0) {
+    atomicAdd(&red[stage].phase[0], (unsigned long long)tc);
+    atomicAdd(&red[stage].phase[1], (unsigned long long)tp);
+    atomicAdd(&red[stage].phase[2], (unsigned long long)tr);
+  }
+}
+
 }  // namespace
 
 // slab / nslab / S: k-slab pipelining (pmhd_gpu.cu): slab q covers k planes
@@ -457,6 +643,39 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
       nt0 = a;
       nt1 = e;
     }
+  }
+  // x2 / x3 faces: the column-march kernel with PMHD_FLUX_MARCH=1 (measured
+  // at 256^3: 7.80 ms per cycle at 4 CTAs/SM against 7.79 for the tile
+  // kernel; 7.93 at 5 CTAs/SM with spills; 64-face segments 8.08-8.11)
+  const char* me = std::getenv("PMHD_FLUX_MARCH");  // (read per launch: tests switch it)
+  const bool march_on = me && std::atoi(me) != 0;
+  if (dir >= 1 && march_on && nslab == 1) {
+    // march axis m: j for x2, k for x3; transverse t: k for x2, j for x3
+    const int m0 = (dir == 2) ? k0 : j0, m1 = (dir == 2) ? k1 : j1;
+    const int t0 = (dir == 2) ? j0 : k0, t1 = (dir == 2) ? j1 : k1;
+    const int nm = (m1 - m0 + PMHD_MARCH_L - 1) / PMHD_MARCH_L;
+    const dim3 mg((i1 - i0 + 31) / 32, (t1 - t0 + 3) / 4, nm * G.nb);
+#define PMHD_MARCH_LAUNCH(D, R, M) \
+  k_flux_march<D, R, M><<<mg, MT, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red, write_ec, i0, i1, m0, m1, \
+                                          t0, t1, region, reuse)
+#define PMHD_MARCH_MODES(D, R)                                     \
+  do {                                                             \
+    if (kd) PMHD_MARCH_LAUNCH(D, R, 2);                            \
+    else if (ph.prof) PMHD_MARCH_LAUNCH(D, R, 1);                  \
+    else PMHD_MARCH_LAUNCH(D, R, 0);                               \
+  } while (0)
+#define PMHD_MARCH_DIRS(R)                                         \
+  do {                                                             \
+    if (dir == 1) PMHD_MARCH_MODES(1, R);                          \
+    else PMHD_MARCH_MODES(2, R);                                   \
+  } while (0)
+    if (ph.riemann == PMHD_RIEMANN_HLLE) PMHD_MARCH_DIRS(PMHD_RIEMANN_HLLE);
+    else if (ph.riemann == PMHD_RIEMANN_ROE) PMHD_MARCH_DIRS(PMHD_RIEMANN_ROE);
+    else PMHD_MARCH_DIRS(PMHD_RIEMANN_HLLD);
+#undef PMHD_MARCH_DIRS
+#undef PMHD_MARCH_MODES
+#undef PMHD_MARCH_LAUNCH
+    return;
   }
   const dim3 grid((i1 - i0 + FX - 1) / FX, ty1 - ty0, (nt1 - nt0) * G.nb);
 #define PMHD_FLUX_LAUNCH(D, R)                                                                      \

@@ -46,6 +46,12 @@ constexpr int ECS = PMHD_UPDATE_TMA ? ((EX * EY * 8 + 127) / 128) * 16 : EX * EY
 // recomputed: the cell-centred E ring holds planes k and k+1 (one new plane
 // loaded per step), E1 / E2 at k+1/2 become the k-1/2 values of the next
 // step, and so does the new b3 face at k+1.
+#ifndef PMHD_UPD_FLAT_B
+#define PMHD_UPD_FLAT_B 0  // 1: phase B (E3 + E1 + E2) as one flat item list (spills at 48 regs: 1.79 vs 1.55 ms)
+#endif
+#ifndef PMHD_UPD_FLAT_C
+#define PMHD_UPD_FLAT_C 1  // phase C (b1 + b2 + b3) as one flat item list
+#endif
 #ifndef PMHD_UPDATE_STCS
 #define PMHD_UPDATE_STCS 1  // streaming stores of the new state (+0.25 %)
 #endif
@@ -187,6 +193,43 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       e2s[h][r][c] = e;
     }
   };
+  // Phase B of step k as ONE flat item list (E3 at plane k, then E1 and E2
+  // at k + 1/2 into slot hi), so the 256 threads take ceil(849 / 256) = 4
+  // passes instead of 2 + 2 + 2 with three separate loops; same operands
+  // and expressions as the loops above (3D only).
+  constexpr int NE3 = (UY + 1) * (UX + 1), NE1 = (UY + 1) * UX, NE2 = UY * (UX + 1);
+  auto emf_items = [&](int k, int lo, int hi) {
+    const int kk = k + 1;
+    for (int q = tid; q < NE3 + NE1 + NE2; q += UTHR) {
+      if (q < NE3) {
+        const int c = q % (UX + 1), r = q / (UX + 1);
+        if (c > nx || r > ny) continue;
+        const int id = G.idx(k, j0 + r, i0 + c);
+        PMHD_CHECK_ID(G, id - G.sx);
+        const int ec_c = c + 1, ec_r = r + 1;
+        e3s[r][c] = corner_emf(mode, X1[5][id], X1[5][id - sx], X2[6][id], X2[6][id - 1], X1[7][id],
+                               X1[7][id - sx], X2[7][id], X2[7][id - 1], ec(2, lo)[ec_r][ec_c],
+                               ec(2, lo)[ec_r][ec_c - 1], ec(2, lo)[ec_r - 1][ec_c],
+                               ec(2, lo)[ec_r - 1][ec_c - 1]);
+      } else if (q < NE3 + NE1) {
+        const int q1 = q - NE3, c = q1 % UX, r = q1 / UX;
+        if (c >= nx || r > ny) continue;
+        const int id = G.idx(kk, j0 + r, i0 + c);
+        PMHD_CHECK_ID(G, id - G.sy);
+        PMHD_CHECK_ID(G, id);
+        e1s[hi][r][c] = corner_emf(mode, X2[5][id], X2[5][id - sy], X3[6][id], X3[6][id - sx], X2[7][id],
+                                   X2[7][id - sy], X3[7][id], X3[7][id - sx], ec(0, hi)[r + 1][c + 1],
+                                   ec(0, hi)[r][c + 1], ec(0, lo)[r + 1][c + 1], ec(0, lo)[r][c + 1]);
+      } else {
+        const int q2 = q - NE3 - NE1, c = q2 % (UX + 1), r = q2 / (UX + 1);
+        if (c > nx || r >= ny) continue;
+        const int id = G.idx(kk, j0 + r, i0 + c);
+        e2s[hi][r][c] = corner_emf(mode, X3[5][id], X3[5][id - 1], X1[6][id], X1[6][id - sy], X3[7][id],
+                                   X3[7][id - 1], X1[7][id], X1[7][id - sy], ec(1, hi)[r + 1][c + 1],
+                                   ec(1, lo)[r + 1][c + 1], ec(1, hi)[r + 1][c], ec(1, lo)[r + 1][c]);
+      }
+    }
+  };
   // new b3 on face plane kk from the edge EMFs in slot h
   auto face_b3 = [&](int kk, int h) {
 #pragma unroll
@@ -257,6 +300,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
     else if (d3) load_ec(k + 1);
     __syncthreads();
     // ---- B: E3 at plane k, E1 / E2 at k + 1/2 -------------------------------
+    if (PMHD_UPD_FLAT_B && d3) emf_items(k, lo, hi);
+    else {
 #pragma unroll
     for (int q = tid; q < (UY + 1) * (UX + 1); q += UTHR) {
       const int c = q % (UX + 1), r = q / (UX + 1);
@@ -270,9 +315,61 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
                              ec(2, lo)[ec_r - 1][ec_c - 1]);
     }
     edge_emfs(k + 1, hi);
+    }
     __syncthreads();
     if (tma && k + 2 <= kend) issue_ec(k + 2);  // into slot lo: plane k was last read just above
     if (PROF && tid == 0) { const long long t = clock64(); tph[1] += t - tph[0]; tph[0] = t; }
+#if PMHD_UPD_FLAT_C
+    // ---- C: constrained-transport face update: b1f (faces i0 .. i0+nx),
+    // b2f (faces j0 .. j0+ny) and b3f at face k + 1 (face k carried) as one
+    // flat item list (4 passes of the 256 threads instead of 2 + 2 + 1)
+    constexpr int NB1 = UY * (UX + 1), NB2 = (UY + 1) * UX, NB3 = UY * UX;
+    for (int q = tid; q < NB1 + NB2 + NB3; q += UTHR) {
+      if (q < NB1) {
+        const int c = q % (UX + 1), r = q / (UX + 1);
+        if (c > nx || r >= ny) continue;
+        const int id = G.idx(k, j0 + r, i0 + c);
+        double v;
+        if (d3) v = Sb[5][id] - (c2 * (e3s[r + 1][c] - e3s[r][c]) - c3 * (e2s[hi][r][c] - e2s[lo][r][c]));
+        else v = Sb[5][id] - c2 * (e3s[r + 1][c] - e3s[r][c]);
+        b1s[r][c] = v;
+        if (c < nx || i0 + c == G.ie) {
+          const int i = i0 + c;
+          if (!push || i != G.is) ST(Sout[5] + id, v);
+          if (push) {
+            if (i > G.is && i <= G.is + G.ng) { PMHD_CHECK_ID(G, id + G.mb[0]); ST(PL[5] + id + G.mb[0], v); }
+            if (i >= G.ie - G.ng) { PMHD_CHECK_ID(G, id - G.mb[0]); ST(PR[5] + id - G.mb[0], v); }
+          }
+        }
+      } else if (q < NB1 + NB2) {
+        const int q1 = q - NB1, c = q1 % UX, r = q1 / UX;
+        if (c >= nx || r > ny) continue;
+        const int id = G.idx(k, j0 + r, i0 + c);
+        double v;
+        if (d3) v = Sb[6][id] - (c3 * (e1s[hi][r][c] - e1s[lo][r][c]) - c1 * (e3s[r][c + 1] - e3s[r][c]));
+        else v = Sb[6][id] + c1 * (e3s[r][c + 1] - e3s[r][c]);
+        b2s[r][c] = v;
+        if (r < ny || j0 + r == G.je) {
+          ST(Sout[6] + id, v);
+          if (push) push_cell(6, i0 + c, id, v);
+        }
+      } else {  // face_b3(k + 1, hi) and the store of face k
+        const int q2 = q - NB1 - NB2, c = q2 % UX, r = q2 / UX;
+        if (c >= nx || r >= ny) continue;
+        const int id = G.idx(k, j0 + r, i0 + c);
+        PMHD_CHECK_ID(G, id + sy);
+        const double v = Sb[7][id + sy] - (c1 * (e2s[hi][r][c + 1] - e2s[hi][r][c]) -
+                                          c2 * (e1s[hi][r + 1][c] - e1s[hi][r][c]));
+        b3s[hi][r][c] = v;
+        ST(Sout[7] + id, b3s[lo][r][c]);
+        if (k + 1 == G.ke) ST(Sout[7] + id + sy, v);
+        if (push) {
+          push_cell(7, i0 + c, id, b3s[lo][r][c]);
+          if (k + 1 == G.ke) push_cell(7, i0 + c, id + sy, v);
+        }
+      }
+    }
+#else
     // ---- C: constrained-transport face update -------------------------------
     for (int q = tid; q < UY * (UX + 1); q += UTHR) {  // b1f, faces i0 .. i0+nx
       const int c = q % (UX + 1), r = q / (UX + 1);
@@ -317,6 +414,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
         }
       }
     }
+#endif
     __syncthreads();
 
     // ---- D: conserved update + end-of-stage cons_to_prim + dt --------------
