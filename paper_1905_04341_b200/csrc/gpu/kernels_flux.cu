@@ -178,6 +178,17 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   const int fs0 = f_s0 + (ty0 + blockIdx.y) * FS;  // first face along the 2nd axis
   const DevBlock& B = blks[b];
   double* const* S = B.st[sel];
+  // owned-face reuse: does this tile hold a face (or an E cell) on the rim
+  // of the owned range, i.e. anything with halo images?  (per-tile test;
+  // the per-face test in rim_images then runs on rim tiles only)
+  bool rim = false;
+  if (reuse) {
+    const int s1 = fs0, e1 = fs0 + FS - 1;  // the tile's second-axis range
+    const int fi1 = fi0 + FX - 1;
+    if (DIR == 0) rim = fi0 <= G.is || s1 <= G.js || e1 >= G.je - 1 || (G.dim == 3 && (t3 <= G.ks || t3 >= G.ke - 1));
+    else if (DIR == 1) rim = fi0 <= G.is || fi1 >= G.ie - 1 || s1 <= G.js || (G.dim == 3 && (t3 <= G.ks || t3 >= G.ke - 1));
+    else rim = fi0 <= G.is || fi1 >= G.ie - 1 || t3 <= G.js || t3 >= G.je - 1 || s1 <= G.ks;
+  }
   if (region != 0) {
     // region 1: only tiles whose stencil (cells and the faces their Bcc
     // averages read) avoids everything the ghost exchange writes -- ghost
@@ -234,7 +245,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
         B.ec[0][id] = ev[0];
         B.ec[1][id] = ev[1];
         B.ec[2][id] = ev[2];
-        if (reuse) {  // images on the neighbours' halo columns / rows of the plane
+        if (rim) {  // images on the neighbours' halo columns / rows of the plane
           rim_images<3>(blks, b, G, (DIR == 2) ? 3 : 1, -1, i, j, k, id, ev);
         }
       }
@@ -337,9 +348,9 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       for (int p = 0; p < TS::PER; ++p) {
         if (vmask & (1u << p)) {
           const double q0 = q[p * NTHR];
-          const double dq = plm_slope(q[p * NTHR - TS::DC], q0, q[p * NTHR + TS::DC], ph.limiter);
-          hi[p] = q0 + 0.5 * dq;  // wL of the face above (oracle: qm1 + 0.5*slope)
-          lo[p] = q0 - 0.5 * dq;  // wR of the face below (oracle: q0 - 0.5*slope)
+          const double hdq = plm_half_slope(q[p * NTHR - TS::DC], q0, q[p * NTHR + TS::DC], ph.limiter);
+          hi[p] = q0 + hdq;  // wL of the face above (oracle: qm1 + 0.5*slope)
+          lo[p] = q0 - hdq;  // wR of the face below (oracle: q0 - 0.5*slope)
         }
       }
       __syncthreads();  // all reads of sw[n] done before it is overwritten
@@ -410,7 +421,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     F[6][id] = out[6];
     F[7][id] = out[7];
 #endif
-    if (reuse) {  // a face on the rim of the owned range: its halo images
+    if (rim) {  // a face on the rim of the owned range: its halo images
       rim_images<DIR>(blks, b, G, (G.dim == 3) ? 7 : 3, DIR, i, j, k, id, out);
     }
   }
@@ -541,8 +552,8 @@ k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 #pragma unroll
     for (int n = 0; n < 7; ++n) {
       const double q0 = P[slot(m0 - 1)][n][tid];
-      const double dq = plm_slope(P[slot(m0 - 2)][n][tid], q0, P[slot(m0)][n][tid], ph.limiter);
-      WL[(m0 - 1) & 1][n][tid] = q0 + 0.5 * dq;
+      const double hdq = plm_half_slope(P[slot(m0 - 2)][n][tid], q0, P[slot(m0)][n][tid], ph.limiter);
+      WL[(m0 - 1) & 1][n][tid] = q0 + hdq;
     }
   }
   if (PROF && tid == 0) { const long long c = clock64(); tc += c - tck; tck = c; }
@@ -557,9 +568,9 @@ k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 #pragma unroll
       for (int n = 0; n < 7; ++n) {
         const double q0 = P[slot(f)][n][tid];
-        const double dq = plm_slope(P[slot(f - 1)][n][tid], q0, P[slot(f + 1)][n][tid], ph.limiter);
-        WL[f & 1][n][tid] = q0 + 0.5 * dq;  // wL of face f+1
-        WR[n][tid] = q0 - 0.5 * dq;         // wR of face f
+        const double hdq = plm_half_slope(P[slot(f - 1)][n][tid], q0, P[slot(f + 1)][n][tid], ph.limiter);
+        WL[f & 1][n][tid] = q0 + hdq;  // wL of face f+1
+        WR[n][tid] = q0 - hdq;         // wR of face f
       }
       wlp = &WL[(f - 1) & 1][0][tid];
       wrp = &WR[0][tid];
