@@ -112,11 +112,13 @@ def falg():
 
 def ncu_traffic():
     """Per-launch DRAM bytes of the flux / update kernels at 256^3 from the
-    committed ncu --set full capture (profiles/r01/ncu_traffic_256.json)."""
-    try:
-        return json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic_256.json")))
-    except Exception:
-        return None
+    newest committed ncu --set full capture (profiles/r0N/ncu_traffic_256.json)."""
+    for rnd in ("r02", "r01"):
+        try:
+            return json.load(open(os.path.join(ROOT, "profiles", rnd, "ncu_traffic_256.json")))
+        except Exception:
+            continue
+    return None
 
 
 def fp64_peak():

@@ -211,6 +211,17 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     if (DIR == 0) { i = fi0 - 2 + col; j = fs0 + row; k = t3; }
     else if (DIR == 1) { i = fi0 + col; j = fs0 - 2 + row; k = t3; }
     else { i = fi0 + col; k = fs0 - 2 + row; j = t3; }
+    // donor cell (stage 1) reads only the two cells adjacent to each face:
+    // the outer PLM stencil positions (x1: columns 0, FX+2, FX+3; x2 / x3:
+    // rows 0, FS+2) are skipped -- except row FS+2 when this tile owns that
+    // cell-centred E row (write_ec, owned ranges, last tile)
+    if (!plm) {
+      const int pos = (DIR == 0) ? col : row;
+      if (pos == 0 || pos >= ((DIR == 0) ? FX + 2 : FS + 2)) {
+        const bool ec_row = (DIR != 0) && write_ec && reuse && pos == FS + 2 && fs0 + FS == f_s1;
+        if (!ec_row) return false;
+      }
+    }
     return c < TS::NCELL && i >= 0 && i < G.n1 && j >= 0 && j < G.n2 && k >= 0 && k < G.n3;
   };
   // cons_to_prim of tile cell c (block index id) from its 11 raw values (5
