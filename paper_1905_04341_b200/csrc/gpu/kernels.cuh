@@ -140,6 +140,9 @@ void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir,
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
                        int plm, double c1024, const KStage* kd, int stage, DevRed* red, int slab,
                        int nslab, int S, cudaStream_t s, int region = 0, int reuse = 0);
+// x1 and x2 faces in one launch (owned-face ranges; kernels_flux.cu k_flux_xy)
+void launch_flux_xy(const DevBlock* blks, const KGeom& G, const KPhys& ph, int sel, int plm, double c1024x,
+                    double c1024y, const KStage* kd, int stage, DevRed* red, cudaStream_t s);
 void launch_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, cudaStream_t s);
 // ec_maps (optional, 3D meshes): per block, TMA tensor maps of its 3 cell-E
 // arrays (box = the update tile's E box) -- the kernel then streams its E

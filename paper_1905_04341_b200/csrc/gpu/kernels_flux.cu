@@ -18,7 +18,10 @@
 // The last direction's kernel also writes the cell-centred E = -v x B of the
 // box the fused update kernel needs (cells [is-1,ie] x [js-1,je] x [ks-1,ke]),
 // so that kernel does not redo cons_to_prim.
+#include <algorithm>
+#include <atomic>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -34,6 +37,9 @@ namespace {
 #endif
 #ifndef PMHD_P1_BATCH
 #define PMHD_P1_BATCH 3  // stencil cells whose loads are batched per thread
+#endif
+#ifndef PMHD_PLM_GROUP
+#define PMHD_PLM_GROUP 1  // PLM variables per in-place barrier (7: one for all -- measured equal)
 #endif
 #ifndef PMHD_FLUX_X1_FX
 #define PMHD_FLUX_X1_FX 32  // x1 tiles: faces along i
@@ -340,6 +346,9 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   if (PROF && threadIdx.x == 0) tph[1] = clock64();
 
   // ---- phase 2: per-cell reconstruction, one variable at a time ------------
+#ifdef PMHD_DIAG_NO_PLM  // diagnostic build only: donor-cell states in stage 2 too
+  plm = 0;
+#endif
   if (plm) {
     constexpr int LEN = (DIR == 0) ? TS::NCOL : TS::NROW;
     // which of this thread's cells have both stencil neighbours in the tile
@@ -351,26 +360,38 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       const int pos = (DIR == 0) ? c % TS::NCOL : c / TS::NCOL;
       if (c < TS::NCELL && pos >= 1 && pos <= LEN - 2) vmask |= 1u << p;
     }
-#pragma unroll 1
-    for (int n = 0; n < 7; ++n) {
-      double lo[TS::PER], hi[TS::PER];
-      double* const q = &sw[n][threadIdx.x];
+    // The high-face values go to sp, which phase 2 does not read, so they are
+    // stored at once; the low-face values overwrite sw in place, so they wait
+    // in registers until every thread has read the group's variables: one
+    // barrier per PMHD_PLM_GROUP variables (7: one for all; the phase runs
+    // before the Riemann solver's registers are live).
+    constexpr int GRP = PMHD_PLM_GROUP;
 #pragma unroll
-      for (int p = 0; p < TS::PER; ++p) {
-        if (vmask & (1u << p)) {
-          const double q0 = q[p * NTHR];
-          const double hdq = plm_half_slope(q[p * NTHR - TS::DC], q0, q[p * NTHR + TS::DC], ph.limiter);
-          hi[p] = q0 + hdq;  // wL of the face above (oracle: qm1 + 0.5*slope)
-          lo[p] = q0 - hdq;  // wR of the face below (oracle: q0 - 0.5*slope)
+    for (int n0 = 0; n0 < 7; n0 += GRP) {
+      double lo[GRP][TS::PER];
+#pragma unroll
+      for (int g = 0; g < GRP; ++g) {
+        const int n = n0 + g;
+        if (n >= 7) break;
+        const double* const q = &sw[n][threadIdx.x];
+#pragma unroll
+        for (int p = 0; p < TS::PER; ++p) {
+          if (vmask & (1u << p)) {
+            const double q0 = q[p * NTHR];
+            const double hdq = plm_half_slope(q[p * NTHR - TS::DC], q0, q[p * NTHR + TS::DC], ph.limiter);
+            sp[n][threadIdx.x + p * NTHR] = q0 + hdq;  // wL of the face above (oracle: qm1 + 0.5*slope)
+            lo[g][p] = q0 - hdq;                       // wR of the face below (oracle: q0 - 0.5*slope)
+          }
         }
       }
-      __syncthreads();  // all reads of sw[n] done before it is overwritten
+      __syncthreads();  // all reads of the group's sw[n] done before they are overwritten
 #pragma unroll
-      for (int p = 0; p < TS::PER; ++p) {
-        if (vmask & (1u << p)) {
-          q[p * NTHR] = lo[p];
-          sp[n][threadIdx.x + p * NTHR] = hi[p];
-        }
+      for (int g = 0; g < GRP; ++g) {
+        const int n = n0 + g;
+        if (n >= 7) break;
+#pragma unroll
+        for (int p = 0; p < TS::PER; ++p)
+          if (vmask & (1u << p)) sw[n][threadIdx.x + p * NTHR] = lo[g][p];
       }
     }
     __syncthreads();
@@ -413,6 +434,10 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     if (fb)
       atomicAdd(&red[stage].fallback_count, 1ULL);
     double* const* F = B.fx[DIR];
+#ifdef PMHD_DIAG_NO_FACE_STORES  // diagnostic build only: skip the face-data stores
+    if (out[0] == 12345.678) F[0][id] = out[1];  // (keeps the solve live)
+    continue;
+#endif
 #if PMHD_FLUX_STCS  // streaming stores: the face data is read back by the next kernel, not reused here
     __stcs(F[0] + id, out[0]);
     __stcs(F[rot_var<DIR>(1)] + id, out[1]);
@@ -449,7 +474,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 
 //---------------------------------------------------------------------------
 // Column-march flux kernel for the x2 and x3 faces (DIR 1: march along j,
-// DIR 2: march along k).  Their stencil runs along an axis the threads of a
+// DIR 2: march along k; the default for them).  Their stencil runs along an axis the threads of a
 // warp do not share (a warp is 32 consecutive i), so each thread owns one
 // face column and walks it: per step it loads and converts ONE new cell,
 // forms ONE PLM slope and solves ONE face, keeping the last three cells'
@@ -457,12 +482,18 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 // shared memory ([var][thread], conflict-free; HLLD reads its side states
 // from there through SmemW as in k_flux_fused).  No thread reads another
 // thread's data, so there is no __syncthreads at all, and a column segment
-// of L faces converts L + 3 cells (the tile kernel: 1.19 per face).  Same
-// expressions and operand order as k_flux_fused, so the same bits.
+// of L faces converts L + 3 cells (the tile kernel: 1.19 per face), and the
+// next cell's raw values are loaded one step ahead into registers, so their
+// latency hides behind the current face's solve (the tile kernel cannot:
+// its loads precede a CTA barrier).  Same expressions and operand order as
+// k_flux_fused, so the same bits.
 #ifndef PMHD_MARCH_L
-#define PMHD_MARCH_L 32  // faces per column segment
+#define PMHD_MARCH_L 24  // faces per column segment (measured: 16 / 24 / 32 / 48 -> 7.60 / 7.56 / 7.60 / 7.58 ms)
 #endif
 constexpr int MT = 128;  // threads: 32 i x 4 transverse columns
+#ifndef PMHD_MARCH_PREFETCH
+#define PMHD_MARCH_PREFETCH 1  // load the next cell's raw values one step ahead
+#endif
 #ifndef PMHD_MARCH_MINB
 #define PMHD_MARCH_MINB 4  // CTAs per SM the registers are sized for (5 spills 24-32 B)
 #endif
@@ -508,12 +539,12 @@ k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   auto cid = [&](int m) { return (DIR == 2) ? G.idx(m, t, i) : G.idx(t, m, i); };
   // load + cons_to_prim of the cell at march position m into ring slot sl
   // (and its cell-centred E where this segment owns it)
-  auto cell = [&](int m, int sl) {
-    const bool in = (m >= 0 && m < ((DIR == 2) ? G.n3 : G.n2));
-    if (!in) return;
+  auto in_range = [&](int m) { return m >= 0 && m < ((DIR == 2) ? G.n3 : G.n2); };
+  // the cell's 11 raw values (5 conserved, then the face pairs)
+  auto load_raw = [&](int m, double* ub) {
+    if (!in_range(m)) return;
     const int id = cid(m);
     PMHD_CHECK_ID(G, id + G.sy);
-    double ub[11];
 #pragma unroll
     for (int v = 0; v < 5; ++v) ub[v] = __ldg(S[v] + id);
     ub[5] = __ldg(S[5] + id);
@@ -522,6 +553,11 @@ k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     ub[8] = __ldg(S[6] + id + G.sx);
     ub[9] = __ldg(S[7] + id);
     ub[10] = __ldg(S[7] + id + G.sy);
+  };
+  // cons_to_prim of the cell at march position m from its raw values
+  auto conv = [&](int m, int sl, const double* ub) {
+    if (!in_range(m)) return;
+    const int id = cid(m);
     double u[5], bc[3], w[8];
 #pragma unroll
     for (int v = 0; v < 5; ++v) u[v] = ub[v];
@@ -550,6 +586,11 @@ k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 #pragma unroll
     for (int n = 0; n < 7; ++n) P[sl][n][tid] = w[rot_var<DIR>(n)];
   };
+  auto cell = [&](int m, int sl) {
+    double ub[11];
+    load_raw(m, ub);
+    conv(m, sl, ub);
+  };
   const double c1024 = (MODE == 2) ? kd->c1024[DIR] : c1024_arg;
   // prologue: cells m0-2, m0-1 (donor: m0-1 is the first face's low side;
   // PLM: both feed the first slope), ring slot = position mod 3
@@ -568,10 +609,19 @@ k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     }
   }
   if (PROF && tid == 0) { const long long c = clock64(); tc += c - tck; tck = c; }
+  // the raw values of the next cell a step converts are loaded one step
+  // ahead (PMHD_MARCH_PREFETCH), so their latency hides behind the solve
+  const int ahead = plm ? 1 : 0;  // step f converts cell f + ahead
+  double pre[11];
+  if (PMHD_MARCH_PREFETCH) load_raw(m0 + ahead, pre);
   for (int f = m0; f < m1; ++f) {
     // cell f (donor) / f+1 (PLM) -- the last one the face at f needs
-    if (plm) cell(f + 1, slot(f + 1));
-    else cell(f, slot(f));
+    if (PMHD_MARCH_PREFETCH) {
+      conv(f + ahead, slot(f + ahead), pre);
+      if (f + 1 < m1) load_raw(f + 1 + ahead, pre);
+    } else {
+      cell(f + ahead, slot(f + ahead));
+    }
     if (PROF && tid == 0) { const long long c = clock64(); tc += c - tck; tck = c; }
     const double* wlp;
     const double* wrp;
@@ -631,6 +681,192 @@ k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   }
 }
 
+//---------------------------------------------------------------------------
+// x1 + x2 flux kernel (owned-face ranges only): one 32 x 16 tile of x1 AND
+// x2 faces in one k-plane.  The flux kernels spend most of their time on
+// loading, converting and reconstructing stencil cells and storing faces
+// (with the Riemann solver replaced by a central flux a launch still takes
+// 80 % of its time), so the two in-plane directions
+// share one load + cons_to_prim of the union stencil (704 cells for 1024
+// faces; separate x1 / x2 tiles convert 1184).  The PLM writes its interface
+// values to a separate buffer (R) instead of in place, so a direction's
+// reconstruction needs one barrier instead of one per variable.  Same
+// expressions and operands as k_flux_fused: the same bits.
+constexpr int XY_FX = 32, XY_FY = 16;          // faces per tile along i, j
+constexpr int XY_NC = XY_FX + 4, XY_NR = XY_FY + 4;  // cell tile 36 x 20 (i0-2.., j0-2..)
+constexpr int XY_NCELL = XY_NC * XY_NR;
+constexpr int XY_R1 = (XY_FX + 1) * XY_FY;    // x1 reconstruction cells: i0-1..i0+31 x j0..j0+15
+constexpr int XY_R2 = XY_FX * (XY_FY + 1);    // x2 reconstruction cells: i0..i0+31 x j0-1..j0+15
+constexpr int XY_RS = XY_R2 > XY_R1 ? XY_R2 : XY_R1;
+constexpr int XY_T = 256;
+// side states in lab-order primitives, read in the rotated order of DIR
+template <int DIR>
+struct RotW {
+  const volatile double* p;
+  int s;
+  PMHD_DEV double operator[](int n) const { return p[rot_var<DIR>(n) * s]; }
+};
+
+template <int RS, int MODE>
+__global__ void __launch_bounds__(XY_T, 2)
+k_flux_xy(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024x, double c1024y,
+          const KStage* __restrict__ kd, int stage, DevRed* red, int write_ec) {
+  constexpr bool PROF = (MODE == 1);
+  if (MODE == 2 && kd->skip) return;
+  extern __shared__ __align__(16) double xy_smem[];
+  double* P = xy_smem;                  // [8][XY_NCELL] lab-order primitives
+  double* R = xy_smem + 8 * XY_NCELL;   // [14][XY_RS]: 0..6 low-face (wR), 7..13 high-face (wL) values
+  __shared__ long long tph[4];
+  const int tid = threadIdx.x;
+  if (PROF && tid == 0) tph[0] = clock64();
+  const int nk = G.ke - G.ks;
+  const int b = blockIdx.z / nk;
+  const int k = G.ks + (int)(blockIdx.z % nk);
+  const int fi0 = G.is + blockIdx.x * XY_FX, fj0 = G.js + blockIdx.y * XY_FY;
+  const DevBlock& B = blks[b];
+  double* const* S = B.st[sel];
+  const bool rim = fi0 <= G.is || fi0 + XY_FX - 1 >= G.ie - 1 || fj0 <= G.js || fj0 + XY_FY - 1 >= G.je - 1 ||
+                   (G.dim == 3 && (k <= G.ks || k >= G.ke - 1));
+  // ---- phase 1: load + cons_to_prim of the union stencil ------------------
+  // tile cell c = r * 36 + col <-> (i0 - 2 + col, j0 - 2 + r); PLM needs the
+  // 16 main rows over all 36 columns and the 2 + 2 halo rows over the 32
+  // face columns; donor cell the cells next to the faces only
+  auto cell_ij = [&](int c, int& i, int& j) {
+    const int col = c % XY_NC, row = c / XY_NC;
+    i = fi0 - 2 + col;
+    j = fj0 - 2 + row;
+    const bool main_row = row >= 2 && row < XY_NR - 2;
+    bool need;
+    if (plm) need = main_row || (col >= 2 && col < XY_NC - 2);
+    else {
+      need = (main_row && col >= 1 && col < XY_NC - 2) || (row == 1 && col >= 2 && col < XY_NC - 2);
+      // the cell-centred E row above the last face row (2D, last tile)
+      if (write_ec && row == XY_NR - 2 && col >= 2 && col < XY_NC - 2 && fj0 + XY_FY == G.je) need = true;
+    }
+    return c < XY_NCELL && need && i >= 0 && i < G.n1 && j >= 0 && j < G.n2;
+  };
+  auto finish = [&](int c, int id, const double* ub) {
+    double u[5], bc[3], w[8];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = ub[v];
+    bc[0] = 0.5 * (ub[5] + ub[6]);
+    bc[1] = 0.5 * (ub[7] + ub[8]);
+    bc[2] = 0.5 * (ub[9] + ub[10]);
+    const int fl = cons_to_prim(u, bc, ph, w, false);
+    int i, j;
+    cell_ij(c, i, j);
+    if ((fl & 4) && k >= G.ks && k < G.ke && j >= G.js && j < G.je && i >= G.is && i < G.ie) {
+      const long long gi = (long long)B.c[0] * G.mb[0] + (i - G.is);
+      const long long gj = (long long)B.c[1] * G.mb[1] + (j - G.js);
+      const long long gk = (G.dim == 3) ? (long long)B.c[2] * G.mb[2] + (k - G.ks) : 0;
+      atomicMin(&red[stage].bad_key, (unsigned long long)((gk * G.nx[1] + gj) * G.nx[0] + gi));
+    }
+    if (write_ec) {  // 2D: this kernel is the last direction (rows js-1 .. je)
+      const bool own = (j >= fj0 && j < fj0 + XY_FY) || (fj0 == G.js && j == G.js - 1) ||
+                       (j == G.je && fj0 + XY_FY >= G.je);
+      if (own && i >= G.is && i < G.ie) {
+        const double ev[3] = {w[3] * w[6] - w[2] * w[7], w[1] * w[7] - w[3] * w[5], w[2] * w[5] - w[1] * w[6]};
+        B.ec[0][id] = ev[0];
+        B.ec[1][id] = ev[1];
+        B.ec[2][id] = ev[2];
+        if (rim) rim_images<3>(blks, b, G, 1, -1, i, j, k, id, ev);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 8; ++v) P[v * XY_NCELL + c] = w[v];
+  };
+  constexpr int PER = (XY_NCELL + XY_T - 1) / XY_T;
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int c = tid + p * XY_T;
+    int i, j;
+    if (!cell_ij(c, i, j)) continue;
+    const int id = G.idx(k, j, i);
+    PMHD_CHECK_ID(G, id + G.sy);
+    double ub[11];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) ub[v] = __ldg(S[v] + id);
+    ub[5] = __ldg(S[5] + id);
+    ub[6] = __ldg(S[5] + id + 1);
+    ub[7] = __ldg(S[6] + id);
+    ub[8] = __ldg(S[6] + id + G.sx);
+    ub[9] = __ldg(S[7] + id);
+    ub[10] = __ldg(S[7] + id + G.sy);
+    finish(c, id, ub);
+  }
+  __syncthreads();
+  if (PROF && tid == 0) tph[1] = clock64();
+  long long trec = 0, trie = 0;
+
+  // one direction: reconstruct (stage 2) then solve the tile's 512 faces
+  auto direction = [&](auto dir_tag, double c1024) {
+    constexpr int DIR = decltype(dir_tag)::value;
+    constexpr int DC = (DIR == 0) ? 1 : XY_NC;     // stencil stride in the cell tile
+    constexpr int NRC = (DIR == 0) ? XY_R1 : XY_R2;
+    long long t0 = 0;
+    if (PROF && tid == 0) t0 = clock64();
+    if (plm) {
+      for (int q = tid; q < NRC; q += XY_T) {
+        // reconstruction cell q -> tile cell
+        const int c = (DIR == 0) ? (q / (XY_FX + 1) + 2) * XY_NC + (q % (XY_FX + 1)) + 1
+                                 : (q / XY_FX + 1) * XY_NC + (q % XY_FX) + 2;
+#pragma unroll
+        for (int n = 0; n < 7; ++n) {
+          const double* pv = P + rot_var<DIR>(n) * XY_NCELL + c;
+          const double q0 = pv[0];
+          const double hdq = plm_half_slope(pv[-DC], q0, pv[DC], ph.limiter);
+          R[n * XY_RS + q] = q0 - hdq;        // wR of the face below
+          R[(7 + n) * XY_RS + q] = q0 + hdq;  // wL of the face above
+        }
+      }
+      __syncthreads();
+    }
+    if (PROF && tid == 0) { const long long t = clock64(); trec += t - t0; t0 = t; }
+    double* const* F = B.fx[DIR];
+    for (int h = 0; h < 2; ++h) {
+      const int fq = tid + XY_T * h;  // face in the tile: 32 along i, 16 along j
+      const int fc = fq % XY_FX, fr = fq / XY_FX;
+      const int i = fi0 + fc, j = fj0 + fr;
+      if (i >= G.ie || j >= G.je) continue;
+      const int id = G.idx(k, j, i);
+      PMHD_CHECK_ID(G, id);
+      const double bn = __ldg(S[5 + DIR] + id);
+      double out[8];
+      int fb;
+      if (plm) {
+        // reconstruction cells of the face's low / high sides
+        const int ql = (DIR == 0) ? fr * (XY_FX + 1) + fc : fr * XY_FX + fc;
+        const int qh = (DIR == 0) ? ql + 1 : ql + XY_FX;
+        const SmemW wl{R + 7 * XY_RS + ql, XY_RS}, wr{R + qh, XY_RS};
+        fb = face_solve<RS>(wl, wr, bn, ph, c1024, out);
+      } else {
+        const int ch = (fr + 2) * XY_NC + fc + 2, cl = ch - DC;
+        const RotW<DIR> wl{P + cl, XY_NCELL}, wr{P + ch, XY_NCELL};
+        fb = face_solve<RS>(wl, wr, bn, ph, c1024, out);
+      }
+      if (fb) atomicAdd(&red[stage].fallback_count, 1ULL);
+      __stcs(F[0] + id, out[0]);
+      __stcs(F[rot_var<DIR>(1)] + id, out[1]);
+      __stcs(F[rot_var<DIR>(2)] + id, out[2]);
+      __stcs(F[rot_var<DIR>(3)] + id, out[3]);
+      __stcs(F[4] + id, out[4]);
+      __stcs(F[5] + id, out[5]);
+      __stcs(F[6] + id, out[6]);
+      __stcs(F[7] + id, out[7]);
+      if (rim) rim_images<DIR>(blks, b, G, (G.dim == 3) ? 7 : 3, DIR, i, j, k, id, out);
+    }
+    if (PROF && tid == 0) trie += clock64() - t0;
+  };
+  direction(std::integral_constant<int, 0>{}, (MODE == 2) ? kd->c1024[0] : c1024x);
+  if (plm) __syncthreads();  // R is refilled by x2
+  direction(std::integral_constant<int, 1>{}, (MODE == 2) ? kd->c1024[1] : c1024y);
+  if (PROF && tid == 0) {
+    atomicAdd(&red[stage].phase[0], (unsigned long long)(tph[1] - tph[0]));
+    atomicAdd(&red[stage].phase[1], (unsigned long long)trec);
+    atomicAdd(&red[stage].phase[2], (unsigned long long)trie);
+  }
+}
+
 }  // namespace
 
 // slab / nslab / S: k-slab pipelining (pmhd_gpu.cu): slab q covers k planes
@@ -666,11 +902,12 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
       nt1 = e;
     }
   }
-  // x2 / x3 faces: the column-march kernel with PMHD_FLUX_MARCH=1 (measured
-  // at 256^3: 7.80 ms per cycle at 4 CTAs/SM against 7.79 for the tile
-  // kernel; 7.93 at 5 CTAs/SM with spills; 64-face segments 8.08-8.11)
+  // x2 / x3 faces: the column-march kernel (PMHD_FLUX_MARCH=0: the tile
+  // kernel).  Measured at 256^3 per cycle: 7.56 ms against 7.73 for the tile
+  // kernel with the next cell's raw values prefetched one step ahead; 7.80
+  // without the prefetch (4 CTAs/SM), 7.93 at 5 CTAs/SM (spills)
   const char* me = std::getenv("PMHD_FLUX_MARCH");  // (read per launch: tests switch it)
-  const bool march_on = me && std::atoi(me) != 0;
+  const bool march_on = !(me && std::atoi(me) == 0);
   if (dir >= 1 && march_on && nslab == 1) {
     // march axis m: j for x2, k for x3; transverse t: k for x2, j for x3
     const int m0 = (dir == 2) ? k0 : j0, m1 = (dir == 2) ? k1 : j1;
@@ -700,16 +937,21 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
     return;
   }
   const dim3 grid((i1 - i0 + FX - 1) / FX, ty1 - ty0, (nt1 - nt0) * G.nb);
+  // experiment knob (PMHD_FLUX_SMEM_PAD = bytes of unused dynamic shared
+  // memory per CTA): caps the flux CTAs per SM so that an update CTA of a
+  // concurrent stream can co-reside (k-slab pipeline study)
+  int pad = 0;
+  if (const char* e = std::getenv("PMHD_FLUX_SMEM_PAD")) pad = std::max(0, std::atoi(e)) + (dir == 0 ? 1792 : 0);
 #define PMHD_FLUX_LAUNCH(D, R)                                                                      \
   do {                                                                                              \
     if (kd)                                                                                         \
-      k_flux_fused<D, R, 2><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
+      k_flux_fused<D, R, 2><<<grid, NTHR, pad, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
                                                   write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region, reuse); \
     else if (ph.prof)                                                                               \
-      k_flux_fused<D, R, 1><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
+      k_flux_fused<D, R, 1><<<grid, NTHR, pad, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
                                                   write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region, reuse); \
     else                                                                                            \
-      k_flux_fused<D, R, 0><<<grid, NTHR, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
+      k_flux_fused<D, R, 0><<<grid, NTHR, pad, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red,     \
                                                   write_ec, i0, i1, ns0, ns1, nt0, nt1, ty0, region, reuse); \
   } while (0)
 #define PMHD_FLUX_DIRS(R)                          \
@@ -723,6 +965,33 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   else PMHD_FLUX_DIRS(PMHD_RIEMANN_HLLD);
 #undef PMHD_FLUX_DIRS
 #undef PMHD_FLUX_LAUNCH
+}
+
+// x1 + x2 faces in one launch (owned-face ranges only; see k_flux_xy)
+void launch_flux_xy(const DevBlock* blks, const KGeom& G, const KPhys& ph, int sel, int plm, double c1024x,
+                    double c1024y, const KStage* kd, int stage, DevRed* red, cudaStream_t s) {
+  const int write_ec = (G.dim == 2) ? 1 : 0;
+  const dim3 grid((G.ie - G.is + XY_FX - 1) / XY_FX, (G.je - G.js + XY_FY - 1) / XY_FY, (G.ke - G.ks) * G.nb);
+  constexpr int smem = (8 * XY_NCELL + 14 * XY_RS) * 8;
+#define PMHD_XY_LAUNCH(R)                                                                               \
+  do {                                                                                                  \
+    static std::atomic<unsigned long long> attr_devs{0};                                                \
+    int dev = 0;                                                                                        \
+    cudaGetDevice(&dev);                                                                                \
+    if (!(attr_devs.load() & (1ULL << (dev & 63)))) {                                                   \
+      cudaFuncSetAttribute(k_flux_xy<R, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
+      cudaFuncSetAttribute(k_flux_xy<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
+      cudaFuncSetAttribute(k_flux_xy<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
+      attr_devs.fetch_or(1ULL << (dev & 63));                                                           \
+    }                                                                                                   \
+    if (kd) k_flux_xy<R, 2><<<grid, XY_T, smem, s>>>(blks, G, ph, sel, plm, c1024x, c1024y, kd, stage, red, write_ec); \
+    else if (ph.prof) k_flux_xy<R, 1><<<grid, XY_T, smem, s>>>(blks, G, ph, sel, plm, c1024x, c1024y, kd, stage, red, write_ec); \
+    else k_flux_xy<R, 0><<<grid, XY_T, smem, s>>>(blks, G, ph, sel, plm, c1024x, c1024y, kd, stage, red, write_ec); \
+  } while (0)
+  if (ph.riemann == PMHD_RIEMANN_HLLE) PMHD_XY_LAUNCH(PMHD_RIEMANN_HLLE);
+  else if (ph.riemann == PMHD_RIEMANN_ROE) PMHD_XY_LAUNCH(PMHD_RIEMANN_ROE);
+  else PMHD_XY_LAUNCH(PMHD_RIEMANN_HLLD);
+#undef PMHD_XY_LAUNCH
 }
 
 }  // namespace pmhd_gpu

@@ -307,6 +307,15 @@ KStage make_stage(const KGeom& G, int s, double dt) {
 
 bool can_prefetch(const pmhd_mesh* m) { return m->overlap && m->variant == 0 && !m->prof; }
 
+// x1 and x2 faces in one k_flux_xy launch (PMHD_FLUX_XY=1): owned-face
+// ranges only (the two directions then share one tile grid); read per stage
+// (tests switch it)
+bool use_flux_xy(const pmhd_mesh* m) {
+  if (m->variant != 0 || !m->face_reuse) return false;
+  const char* e = std::getenv("PMHD_FLUX_XY");
+  return e && std::atoi(e) != 0;  // opt-in: measured 6.6 % slower at 256^3 (16 warps/SM)
+}
+
 // Interior flux tiles of stage s on stream2, after the work already on the
 // main stream (the update that produced their input); the ghost exchange that
 // follows on the main stream runs concurrently (the tiles read no ghost data).
@@ -379,7 +388,9 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     rec(m, 0);
     if (m->variant == 1) launch_c2p_all(m->dblk, G, m->ph, ks.in_sel, m->dred, s, st);
     rec(m, 1);
-    for (int dir = 0; dir < G.dim; ++dir) {
+    const bool xy = use_flux_xy(m) && flux_region == 0;
+    if (xy) launch_flux_xy(m->dblk, G, m->ph, ks.in_sel, ks.plm, ks.c1024[0], ks.c1024[1], kd, s, m->dred, st);
+    for (int dir = xy ? 2 : 0; dir < G.dim; ++dir) {
       if (m->variant == 0)
         launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], kd, s, m->dred, 0, 1,
                           nk, st, flux_region, m->face_reuse ? 1 : 0);
@@ -405,7 +416,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     if (do_exchange)
       for (int dir = d0; dir < G.dim; ++dir) launch_exchange_dir(m->dblk, G, ks.out_sel, dir, st, kd);
     rec(m, 5);
-    m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim : 4 + G.dim) + (do_exchange ? G.dim - d0 : 0);
+    m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim - (xy ? 1 : 0) : 4 + G.dim) + (do_exchange ? G.dim - d0 : 0);
   }
   CK(cudaGetLastError());
   if (s == 2) {  // u^{n+1} (st[2]) becomes the current state: flip the tables
@@ -995,7 +1006,7 @@ int graph_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int
   // cycles that ran: the completed ones, plus the failing one (its stages ran
   // and flipped the tables inside the graph)
   const int ran = c.cycles + (c.err_key != ULLONG_MAX ? 1 : 0);
-  const long long per_cycle = 2 + 2 * (2 * G.dim + 1 - (m->push_x1 ? 1 : 0));
+  const long long per_cycle = 2 + 2 * (2 * G.dim + 1 - (m->push_x1 ? 1 : 0) - (use_flux_xy(m) ? 1 : 0));
   m->times.kernel_launches += per_cycle * ran;
   if (ran & 1) {  // the state is in the other table after an odd number of cycles
     std::swap(m->hblk, m->hblk_alt);

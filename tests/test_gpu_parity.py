@@ -285,12 +285,38 @@ def test_update_kernels_bitwise(gpu_available, case, monkeypatch):
             assert np.array_equal(getattr(b0, f), getattr(b1, f)), (case, f)
 
 
+@pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_ragged", "ot2d_4blk",
+                                  "wave3d_tiny_blocks", "wave3d_ng3_ragged", "wave3d_ng4_8blk", "wave3d_roe",
+                                  "ot2d_roe", "wave3d_hlle_vl_arith", "turb3d"])
+def test_flux_xy_bitwise(gpu_available, case, monkeypatch):
+    """The x1 + x2 flux kernel (PMHD_FLUX_XY=1, owned-face ranges) and the
+    default one launch per direction give the same bits in the parity build,
+    2D (where it also writes the cell-centred E) and 3D."""
+    kw, ncyc = CASES[case]
+    cfg = RunConfig(**kw)
+    out = []
+    for xy in ("0", "1"):
+        monkeypatch.setenv("PMHD_FLUX_XY", xy)
+        g = GpuSolver(cfg, parity=True)
+        g.load_pgen()
+        dt = g.new_dt()
+        dts = []
+        for _ in range(ncyc):
+            dt, _st = g.vl2_step(dt)
+            dts.append(dt)
+        out.append((dts, [g.get_block(gid) for gid in range(cfg.nblocks)]))
+    assert out[0][0] == out[1][0]
+    for b0, b1 in zip(out[0][1], out[1][1]):
+        for f in ("u", "b1f", "b2f", "b3f"):
+            assert np.array_equal(getattr(b0, f), getattr(b1, f)), (case, f)
+
+
 @pytest.mark.parametrize("reuse", ["0", "1"])
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_ragged", "wave3d_tiny_blocks",
                                   "wave3d_ng3_ragged", "wave3d_roe", "wave3d_hlle_vl_arith"])
 def test_flux_kernels_bitwise(gpu_available, case, reuse, monkeypatch):
-    """The column-march x2 / x3 flux kernel (PMHD_FLUX_MARCH=1) and the
-    default tile kernel give the same bits in the parity build, with the
+    """The column-march x2 / x3 flux kernel (default) and the tile kernel
+    (PMHD_FLUX_MARCH=0) give the same bits in the parity build, with the
     owned-face ranges and with the extended ones."""
     kw, ncyc = CASES[case]
     cfg = RunConfig(**kw)

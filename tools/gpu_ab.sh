@@ -8,6 +8,11 @@ for v in "$@"; do
   case $v in
     split) PMHD_KERNELS=split $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     default) $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    ovlpad*) PMHD_FACE_REUSE=0 PMHD_SLAB_PLANES=${v#ovlpad} PMHD_FLUX_SMEM_PAD=11776 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    ovlnr*) PMHD_FACE_REUSE=0 PMHD_SLAB_PLANES=${v#ovlnr} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    xy) PMHD_FLUX_XY=1 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5xy) PMHD_FLUX_XY=1 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    padonly) PMHD_FLUX_SMEM_PAD=11776 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     sh_*) IFS=_ read -r _ a b c <<< "$v"; PMHD_ROW_SHIFT_ST=$a PMHD_ROW_SHIFT_FX=$b PMHD_ROW_SHIFT_EC=$c $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     shift*) PMHD_ROW_SHIFT=${v#shift} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     slab*) PMHD_SLAB_PLANES=${v#slab} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
@@ -15,8 +20,8 @@ for v in "$@"; do
     nooverlap) PMHD_OVERLAP=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     tma) PMHD_UPDATE=tma $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5tma) PMHD_UPDATE=tma $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
-    march) PMHD_FLUX_MARCH=1 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
-    m5march) PMHD_FLUX_MARCH=1 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    tile) PMHD_FLUX_MARCH=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5tile) PMHD_FLUX_MARCH=0 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     noreuse) PMHD_FACE_REUSE=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5) $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5noreuse) PMHD_FACE_REUSE=0 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
@@ -25,6 +30,7 @@ for v in "$@"; do
     hlle|roe) $B --riemann $v > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     *-hlle|*-roe) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_${v%-*}.so $B --riemann ${v##*-} > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     parity) PMHD_GPU_LIB=paper_1905_04341_b200/lib/libpmhd_gpu_parity.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m*) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_$v.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     *) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_$v.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
   esac
   python - "$v" <<'PY'
