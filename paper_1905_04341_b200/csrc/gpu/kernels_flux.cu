@@ -682,6 +682,181 @@ k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
 }
 
 //---------------------------------------------------------------------------
+// Row-march flux kernel for the x1 faces.  Each warp owns one face row (j, k)
+// and walks it in chunks of 32 faces: per chunk every lane loads and converts
+// ONE cell (the one ahead of its face, so the last lane's slope has its right
+// neighbour), the chunk's stencil is shared through a per-warp slice of
+// shared memory (__syncwarp only: warps never wait for each other), each lane
+// forms one PLM slope and solves one face; the two cells and the high-face
+// state the next chunk needs from this one are carried in the slice, and the
+// next chunk's raw values are loaded one chunk ahead into registers.  Same
+// expressions and operand order as k_flux_fused: the same bits.
+constexpr int XT = 128;  // 4 warps = 4 face rows
+template <int RS, int MODE>
+__global__ void __launch_bounds__(XT, MarchMinB<RS>::value)
+k_flux_x1march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm, double c1024_arg,
+               const KStage* __restrict__ kd, int stage, DevRed* red, int f_i0, int f_i1, int f_j0, int f_j1,
+               int f_k0, int f_k1, int region, int reuse) {
+  constexpr bool PROF = (MODE == 1);
+  if (MODE == 2 && kd->skip) return;
+  // per warp: Q[7][34] rotated primitives of cells fb-1 .. fb+32 (fb = the
+  // chunk's first face), HI[7][33] high-face states of cells fb-1 .. fb+31,
+  // LO[7][32] low-face states of cells fb .. fb+31
+  __shared__ double Qs[4][7][34];
+  __shared__ double HIs[4][7][33];
+  __shared__ double LOs[4][7][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nj = f_j1 - f_j0, nrow = nj * (f_k1 - f_k0);
+  const int b = blockIdx.y;
+  const int row = blockIdx.x * 4 + warp;
+  const DevBlock& B = blks[b];
+  double* const* S = B.st[sel];
+  if (region != 0) {  // as k_flux_fused, on the CTA's 4 rows (+ the i stencil)
+    const int r0 = blockIdx.x * 4, r1 = min(r0 + 3, nrow - 1);
+    const int ja = f_j0 + r0 % nj, ka = f_k0 + r0 / nj, jb = f_j0 + r1 % nj, kb = f_k0 + r1 / nj;
+    const int jlo = (ka == kb) ? ja : f_j0, jhi = (ka == kb) ? jb : f_j1 - 1;
+    bool inner = f_i0 - 2 >= G.is + 1 && f_i1 + 1 <= G.ie - 1 && jlo >= G.js + 1 && jhi <= G.je - 1;
+    if (G.dim == 3) inner = inner && ka >= G.ks + 1 && kb <= G.ke - 1;
+    if (inner != (region == 1)) return;
+  }
+  if (row >= nrow) return;  // (warp-uniform; no CTA barriers below)
+  const int j = f_j0 + row % nj, k = f_k0 + row / nj;
+  const bool rim = reuse && (f_i0 <= G.is || j <= G.js || j >= G.je - 1 ||
+                             (G.dim == 3 && (k <= G.ks || k >= G.ke - 1)));
+  double (*Q)[34] = Qs[warp];
+  double (*HI)[33] = HIs[warp];
+  double (*LO)[32] = LOs[warp];
+  long long tc = 0, tp = 0, tr = 0, tck = 0;
+  auto load_raw = [&](int i, double* ub) {
+    if (i < 0 || i >= G.n1) return;
+    const int id = G.idx(k, j, i);
+    PMHD_CHECK_ID(G, id + G.sy);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) ub[v] = __ldg(S[v] + id);
+    ub[5] = __ldg(S[5] + id);
+    ub[6] = __ldg(S[5] + id + 1);
+    ub[7] = __ldg(S[6] + id);
+    ub[8] = __ldg(S[6] + id + G.sx);
+    ub[9] = __ldg(S[7] + id);
+    ub[10] = __ldg(S[7] + id + G.sy);
+  };
+  // cons_to_prim of cell i from its raw values into Q[.][e]
+  auto conv = [&](int i, int e, const double* ub) {
+    if (i < 0 || i >= G.n1) return;
+    double u[5], bc[3], w[8];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) u[v] = ub[v];
+    bc[0] = 0.5 * (ub[5] + ub[6]);
+    bc[1] = 0.5 * (ub[7] + ub[8]);
+    bc[2] = 0.5 * (ub[9] + ub[10]);
+    const int fl = cons_to_prim(u, bc, ph, w, false);
+    if ((fl & 4) && k >= G.ks && k < G.ke && j >= G.js && j < G.je && i >= G.is && i < G.ie) {
+      const long long gi = (long long)B.c[0] * G.mb[0] + (i - G.is);
+      const long long gj = (long long)B.c[1] * G.mb[1] + (j - G.js);
+      const long long gk = (G.dim == 3) ? (long long)B.c[2] * G.mb[2] + (k - G.ks) : 0;
+      atomicMin(&red[stage].bad_key, (unsigned long long)((gk * G.nx[1] + gj) * G.nx[0] + gi));
+    }
+#pragma unroll
+    for (int n = 0; n < 7; ++n) Q[n][e] = w[rot_var<0>(n)];
+  };
+  const double c1024 = (MODE == 2) ? kd->c1024[0] : c1024_arg;
+  if (PROF && lane == 0 && warp == 0) tck = clock64();
+  // ---- prologue: cells fb-2 .. fb (lanes 0..2), then the high-face state of
+  // cell fb-1 (PLM) -- what lane 0 of the first chunk takes from a previous one
+  {
+    double ub[11];
+    const int i = f_i0 - 2 + lane;
+    if (lane < 3) load_raw(i, ub);
+    // (staged through Q[.][lane]: entries 0..2 = cells fb-2, fb-1, fb)
+    if (lane < 3) conv(i, lane, ub);
+    __syncwarp();
+    double q0[7] = {}, q1[7] = {};
+    if (lane == 0) {
+#pragma unroll
+      for (int n = 0; n < 7; ++n) {
+        const double qm = Q[n][0], qc = Q[n][1], qp = Q[n][2];
+        q0[n] = qc;
+        q1[n] = qp;
+        if (plm) HI[n][0] = qc + plm_half_slope(qm, qc, qp, ph.limiter);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int n = 0; n < 7; ++n) {
+        Q[n][0] = q0[n];  // cell fb-1
+        Q[n][1] = q1[n];  // cell fb
+      }
+    }
+  }
+  double pre[11];
+  load_raw(f_i0 + 1 + lane, pre);  // this lane's cell of the first chunk
+  if (PROF && lane == 0 && warp == 0) { const long long c = clock64(); tc += c - tck; tck = c; }
+  double* const* F = B.fx[0];
+  for (int fb = f_i0; fb < f_i1; fb += 32) {
+    // ---- cells fb+1 .. fb+32 (lane l: fb+1+l) into Q[.][2+l]; Q[.][0..1]
+    // hold fb-1, fb (the previous chunk's last two cells)
+    __syncwarp();
+    conv(fb + 1 + lane, 2 + lane, pre);
+    if (fb + 32 < f_i1) load_raw(fb + 33 + lane, pre);  // next chunk, one ahead
+    __syncwarp();
+    if (PROF && lane == 0 && warp == 0) { const long long c = clock64(); tc += c - tck; tck = c; }
+    const int f = fb + lane;  // this lane's face: between cells f-1 (Q[.][lane]) and f (Q[.][lane+1])
+    if (plm) {
+#pragma unroll
+      for (int n = 0; n < 7; ++n) {
+        const double q0 = Q[n][lane + 1];
+        const double hdq = plm_half_slope(Q[n][lane], q0, Q[n][lane + 2], ph.limiter);
+        HI[n][lane + 1] = q0 + hdq;  // wL of face f+1
+        LO[n][lane] = q0 - hdq;      // wR of face f
+      }
+      __syncwarp();
+    }
+    if (PROF && lane == 0 && warp == 0) { const long long c = clock64(); tp += c - tck; tck = c; }
+    if (f < f_i1) {
+      const int id = G.idx(k, j, f);
+      PMHD_CHECK_ID(G, id);
+      const double bn = __ldg(S[5] + id);
+      double out[8];
+      int fb2;
+      if (plm) {
+        const SmemW wl{&HI[0][lane], 33}, wr{&LO[0][lane], 32};
+        fb2 = face_solve<RS>(wl, wr, bn, ph, c1024, out);
+      } else {
+        const SmemW wl{&Q[0][lane], 34}, wr{&Q[0][lane + 1], 34};
+        fb2 = face_solve<RS>(wl, wr, bn, ph, c1024, out);
+      }
+      if (fb2) atomicAdd(&red[stage].fallback_count, 1ULL);
+      __stcs(F[0] + id, out[0]);
+      __stcs(F[1] + id, out[1]);
+      __stcs(F[2] + id, out[2]);
+      __stcs(F[3] + id, out[3]);
+      __stcs(F[4] + id, out[4]);
+      __stcs(F[5] + id, out[5]);
+      __stcs(F[6] + id, out[6]);
+      __stcs(F[7] + id, out[7]);
+      if (rim) rim_images<0>(blks, b, G, (G.dim == 3) ? 7 : 3, 0, f, j, k, id, out);
+    }
+    if (PROF && lane == 0 && warp == 0) { const long long c = clock64(); tr += c - tck; tck = c; }
+    // carry: cells fb+31, fb+32 -> Q[.][0..1]; high-face state of cell fb+31 -> HI[.][0]
+    __syncwarp();
+    if (lane < 2) {
+#pragma unroll
+      for (int n = 0; n < 7; ++n) Q[n][lane] = Q[n][32 + lane];
+    }
+    if (plm && lane == 2) {
+#pragma unroll
+      for (int n = 0; n < 7; ++n) HI[n][0] = HI[n][32];
+    }
+  }
+  if (PROF && lane == 0 && warp == 0) {
+    atomicAdd(&red[stage].phase[0], (unsigned long long)tc);
+    atomicAdd(&red[stage].phase[1], (unsigned long long)tp);
+    atomicAdd(&red[stage].phase[2], (unsigned long long)tr);
+  }
+}
+
+//---------------------------------------------------------------------------
 // x1 + x2 flux kernel (owned-face ranges only): one 32 x 16 tile of x1 AND
 // x2 faces in one k-plane.  The flux kernels spend most of their time on
 // loading, converting and reconstructing stencil cells and storing faces
@@ -908,6 +1083,28 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   // without the prefetch (4 CTAs/SM), 7.93 at 5 CTAs/SM (spills)
   const char* me = std::getenv("PMHD_FLUX_MARCH");  // (read per launch: tests switch it)
   const bool march_on = !(me && std::atoi(me) == 0);
+  // x1 faces: the row-march kernel with PMHD_FLUX_MARCH_X1=1 (measured at
+  // 256^3: 7.574 ms per cycle against 7.566 for the x1 tile kernel)
+  const char* mx = std::getenv("PMHD_FLUX_MARCH_X1");
+  if (dir == 0 && march_on && mx && std::atoi(mx) != 0 && nslab == 1) {
+    const int nrow = (j1 - j0) * (k1 - k0);
+    const dim3 xg((nrow + 3) / 4, G.nb, 1);
+#define PMHD_X1M_LAUNCH(R, M) \
+  k_flux_x1march<R, M><<<xg, XT, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red, i0, i1, j0, j1, k0, k1, \
+                                         region, reuse)
+#define PMHD_X1M_MODES(R)                              \
+  do {                                                 \
+    if (kd) PMHD_X1M_LAUNCH(R, 2);                     \
+    else if (ph.prof) PMHD_X1M_LAUNCH(R, 1);           \
+    else PMHD_X1M_LAUNCH(R, 0);                        \
+  } while (0)
+    if (ph.riemann == PMHD_RIEMANN_HLLE) PMHD_X1M_MODES(PMHD_RIEMANN_HLLE);
+    else if (ph.riemann == PMHD_RIEMANN_ROE) PMHD_X1M_MODES(PMHD_RIEMANN_ROE);
+    else PMHD_X1M_MODES(PMHD_RIEMANN_HLLD);
+#undef PMHD_X1M_MODES
+#undef PMHD_X1M_LAUNCH
+    return;
+  }
   if (dir >= 1 && march_on && nslab == 1) {
     // march axis m: j for x2, k for x3; transverse t: k for x2, j for x3
     const int m0 = (dir == 2) ? k0 : j0, m1 = (dir == 2) ? k1 : j1;

@@ -315,12 +315,14 @@ def test_flux_xy_bitwise(gpu_available, case, monkeypatch):
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_ragged", "wave3d_tiny_blocks",
                                   "wave3d_ng3_ragged", "wave3d_roe", "wave3d_hlle_vl_arith"])
 def test_flux_kernels_bitwise(gpu_available, case, reuse, monkeypatch):
-    """The column-march x2 / x3 flux kernel (default) and the tile kernel
-    (PMHD_FLUX_MARCH=0) give the same bits in the parity build, with the
+    """The column-march x2 / x3 flux kernel (default) with the row-march x1
+    kernel (opt-in) and the tile kernels (PMHD_FLUX_MARCH=0) give the same
+    bits in the parity build, with the
     owned-face ranges and with the extended ones."""
     kw, ncyc = CASES[case]
     cfg = RunConfig(**kw)
     monkeypatch.setenv("PMHD_FACE_REUSE", reuse)
+    monkeypatch.setenv("PMHD_FLUX_MARCH_X1", "1")  # the x1 row march too (opt-in)
     out = []
     for march in ("0", "1"):
         monkeypatch.setenv("PMHD_FLUX_MARCH", march)
