@@ -38,8 +38,8 @@ namespace {
 #ifndef PMHD_P1_BATCH
 #define PMHD_P1_BATCH 3  // stencil cells whose loads are batched per thread
 #endif
-#ifndef PMHD_PLM_GROUP
-#define PMHD_PLM_GROUP 1  // PLM variables per in-place barrier (7: one for all -- measured equal)
+#ifndef PMHD_FLUX_STAGE1_SKIP
+#define PMHD_FLUX_STAGE1_SKIP 1  // stage-1 tiles skip the outer PLM stencil cells
 #endif
 #ifndef PMHD_FLUX_X1_FX
 #define PMHD_FLUX_X1_FX 32  // x1 tiles: faces along i
@@ -221,7 +221,7 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
     // the outer PLM stencil positions (x1: columns 0, FX+2, FX+3; x2 / x3:
     // rows 0, FS+2) are skipped -- except row FS+2 when this tile owns that
     // cell-centred E row (write_ec, owned ranges, last tile)
-    if (!plm) {
+    if (PMHD_FLUX_STAGE1_SKIP && !plm) {
       const int pos = (DIR == 0) ? col : row;
       if (pos == 0 || pos >= ((DIR == 0) ? FX + 2 : FS + 2)) {
         const bool ec_row = (DIR != 0) && write_ec && reuse && pos == FS + 2 && fs0 + FS == f_s1;
@@ -360,38 +360,26 @@ k_flux_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
       const int pos = (DIR == 0) ? c % TS::NCOL : c / TS::NCOL;
       if (c < TS::NCELL && pos >= 1 && pos <= LEN - 2) vmask |= 1u << p;
     }
-    // The high-face values go to sp, which phase 2 does not read, so they are
-    // stored at once; the low-face values overwrite sw in place, so they wait
-    // in registers until every thread has read the group's variables: one
-    // barrier per PMHD_PLM_GROUP variables (7: one for all; the phase runs
-    // before the Riemann solver's registers are live).
-    constexpr int GRP = PMHD_PLM_GROUP;
+#pragma unroll 1
+    for (int n = 0; n < 7; ++n) {
+      double lo[TS::PER], hi[TS::PER];
+      double* const q = &sw[n][threadIdx.x];
 #pragma unroll
-    for (int n0 = 0; n0 < 7; n0 += GRP) {
-      double lo[GRP][TS::PER];
-#pragma unroll
-      for (int g = 0; g < GRP; ++g) {
-        const int n = n0 + g;
-        if (n >= 7) break;
-        const double* const q = &sw[n][threadIdx.x];
-#pragma unroll
-        for (int p = 0; p < TS::PER; ++p) {
-          if (vmask & (1u << p)) {
-            const double q0 = q[p * NTHR];
-            const double hdq = plm_half_slope(q[p * NTHR - TS::DC], q0, q[p * NTHR + TS::DC], ph.limiter);
-            sp[n][threadIdx.x + p * NTHR] = q0 + hdq;  // wL of the face above (oracle: qm1 + 0.5*slope)
-            lo[g][p] = q0 - hdq;                       // wR of the face below (oracle: q0 - 0.5*slope)
-          }
+      for (int p = 0; p < TS::PER; ++p) {
+        if (vmask & (1u << p)) {
+          const double q0 = q[p * NTHR];
+          const double hdq = plm_half_slope(q[p * NTHR - TS::DC], q0, q[p * NTHR + TS::DC], ph.limiter);
+          hi[p] = q0 + hdq;  // wL of the face above (oracle: qm1 + 0.5*slope)
+          lo[p] = q0 - hdq;  // wR of the face below (oracle: q0 - 0.5*slope)
         }
       }
-      __syncthreads();  // all reads of the group's sw[n] done before they are overwritten
+      __syncthreads();  // all reads of sw[n] done before it is overwritten
 #pragma unroll
-      for (int g = 0; g < GRP; ++g) {
-        const int n = n0 + g;
-        if (n >= 7) break;
-#pragma unroll
-        for (int p = 0; p < TS::PER; ++p)
-          if (vmask & (1u << p)) sw[n][threadIdx.x + p * NTHR] = lo[g][p];
+      for (int p = 0; p < TS::PER; ++p) {
+        if (vmask & (1u << p)) {
+          q[p * NTHR] = lo[p];
+          sp[n][threadIdx.x + p * NTHR] = hi[p];
+        }
       }
     }
     __syncthreads();
@@ -1081,8 +1069,10 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   // kernel).  Measured at 256^3 per cycle: 7.56 ms against 7.73 for the tile
   // kernel with the next cell's raw values prefetched one step ahead; 7.80
   // without the prefetch (4 CTAs/SM), 7.93 at 5 CTAs/SM (spills)
-  const char* me = std::getenv("PMHD_FLUX_MARCH");  // (read per launch: tests switch it)
-  const bool march_on = !(me && std::atoi(me) == 0);
+  // (read per launch: tests switch it; 2 forces the march on any mesh size)
+  const char* me = std::getenv("PMHD_FLUX_MARCH");
+  const int march_mode = me ? std::atoi(me) : 1;
+  const bool march_on = march_mode != 0;
   // x1 faces: the row-march kernel with PMHD_FLUX_MARCH_X1=1 (measured at
   // 256^3: 7.574 ms per cycle against 7.566 for the x1 tile kernel)
   const char* mx = std::getenv("PMHD_FLUX_MARCH_X1");
@@ -1105,12 +1095,16 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
 #undef PMHD_X1M_LAUNCH
     return;
   }
-  if (dir >= 1 && march_on && nslab == 1) {
-    // march axis m: j for x2, k for x3; transverse t: k for x2, j for x3
-    const int m0 = (dir == 2) ? k0 : j0, m1 = (dir == 2) ? k1 : j1;
-    const int t0 = (dir == 2) ? j0 : k0, t1 = (dir == 2) ? j1 : k1;
-    const int nm = (m1 - m0 + PMHD_MARCH_L - 1) / PMHD_MARCH_L;
-    const dim3 mg((i1 - i0 + 31) / 32, (t1 - t0 + 3) / 4, nm * G.nb);
+  // march axis m: j for x2, k for x3; transverse t: k for x2, j for x3
+  const int mm0 = (dir == 2) ? k0 : j0, mm1 = (dir == 2) ? k1 : j1;
+  const int mt0 = (dir == 2) ? j0 : k0, mt1 = (dir == 2) ? j1 : k1;
+  const dim3 mg((i1 - i0 + 31) / 32, (mt1 - mt0 + 3) / 4, ((mm1 - mm0 + PMHD_MARCH_L - 1) / PMHD_MARCH_L) * G.nb);
+  // one thread per face column: small meshes (a 64^3 block: 96 CTAs; the
+  // 512^2 Orszag-Tang in 128^2 blocks: 384) cannot fill the GPU that way,
+  // so below two full waves of 148 SMs the tile kernel runs instead
+  const bool march_fills = march_mode == 2 || (long long)mg.x * mg.y * mg.z >= 2LL * 148 * PMHD_MARCH_MINB;
+  if (dir >= 1 && march_on && march_fills && nslab == 1) {
+    const int m0 = mm0, m1 = mm1, t0 = mt0, t1 = mt1;
 #define PMHD_MARCH_LAUNCH(D, R, M) \
   k_flux_march<D, R, M><<<mg, MT, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red, write_ec, i0, i1, m0, m1, \
                                           t0, t1, region, reuse)

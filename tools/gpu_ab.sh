@@ -33,6 +33,7 @@ for v in "$@"; do
     *-hlle|*-roe) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_${v%-*}.so $B --riemann ${v##*-} > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     parity) PMHD_GPU_LIB=paper_1905_04341_b200/lib/libpmhd_gpu_parity.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m*) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_$v.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    r_*) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/$v/libpmhd_gpu.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     *) PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_$v.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
   esac
   python - "$v" <<'PY'
