@@ -366,12 +366,15 @@ def test_face_reuse_bitwise(gpu_available, case, monkeypatch):
             assert np.array_equal(getattr(b0, f), getattr(b1, f)), (case, f)
 
 
+@pytest.mark.parametrize("march", ["1", "2"])
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_4blk"])
-def test_overlap_prefetch_bitwise(gpu_available, case, monkeypatch):
+def test_overlap_prefetch_bitwise(gpu_available, case, march, monkeypatch):
     """Stage-2 interior flux tiles enqueued on a second stream while the
     stage-1 ghost exchange runs (PMHD_OVERLAP=1; on by default only with
-    remote neighbours) are bit-identical to the oracle."""
+    remote neighbours) are bit-identical to the oracle; march "2" forces the
+    column-march x2 / x3 kernels (their region split) on these small meshes."""
     monkeypatch.setenv("PMHD_OVERLAP", "1")
+    monkeypatch.setenv("PMHD_FLUX_MARCH", march)
     kw, ncyc = CASES[case]
     cfg = RunConfig(**kw)
     o, g, _, (fo, fg), dts = run_pair(cfg, ncyc, parity=True)
@@ -422,7 +425,8 @@ MULTIRANK = {
                                                             (2, False, "wave", True), (4, False, "blast", True),
                                                             (4, False, "ot2d", True), (8, False, "blast", True),
                                                             (8, True, "blast", False)])
-def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered, case, p2p):
+@pytest.mark.parametrize("march", ["1", "2"])
+def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered, case, p2p, march, monkeypatch):
     """The multi-rank data path (stage_compute + local sweeps + halo pack /
     unpack kernels + transport) with nranks rank-engines on ONE GPU, stepped in
     lockstep by the host (no kernel waits on another), is bit-identical to the
@@ -430,8 +434,11 @@ def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered, case
     with the hand-over ordered by events between the engines' streams (what
     DistributedVL2 does with NCCL), i.e. no host synchronization in a stage.
     p2p: remote faces read straight from the other engines' memory by the
-    exchange kernels (pmhd_gpu_peer_attach), no pack / unpack."""
+    exchange kernels (pmhd_gpu_peer_attach), no pack / unpack.  march "2":
+    the column-march x2 / x3 kernels forced on these small meshes, so their
+    interior / boundary split (the halo overlap) is covered too."""
     from paper_1905_04341_b200.parallel import plan_for, LoopbackWorld
+    monkeypatch.setenv("PMHD_FLUX_MARCH", march)
     cfg = RunConfig(**MULTIRANK[case])
     plan = plan_for(cfg, nranks)
     engines = [GpuSolver(cfg, parity=True, gids=plan.local_gids(r)) for r in range(nranks)]
