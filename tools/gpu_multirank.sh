@@ -9,3 +9,8 @@ PMHD_BENCH_TRANSPORT=gloo-host timeout 900 python -m torch.distributed.run --nno
   --master-addr 127.0.0.1 --master-port 29555 bench.py --gpus 8 --size 64 --steps 3 --warmup 3 --no-cpu-baseline \
   > gpurun_out/bench_gloo8.json 2> gpurun_out/bench_gloo8.err
 echo "gloo8 rc=$?"; tail -c 900 gpurun_out/bench_gloo8.json; tail -3 gpurun_out/bench_gloo8.err
+# M5 strong-scaling flow at 2 ranks (gloo-host), default kernels
+PMHD_BENCH_TRANSPORT=gloo-host timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29556 bench.py --gpus 2 --workload m5 --steps 3 --warmup 3 --no-cpu-baseline \
+  > gpurun_out/bench_gloo2_m5.json 2> gpurun_out/bench_gloo2_m5.err
+echo "gloo2 m5 rc=$?"; tail -c 600 gpurun_out/bench_gloo2_m5.json; tail -3 gpurun_out/bench_gloo2_m5.err
