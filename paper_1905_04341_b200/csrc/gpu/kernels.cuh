@@ -155,6 +155,9 @@ void update_ec_box(int box[2]);
 // block + id] are the tensor maps of block b for the table the launch uses;
 // bit id of xoffm = 1 when that map starts one element before its array (16 B
 // alignment of the map base).
+// warp-specialised update kernel (kernels_update_ws.cu, 3D)
+void launch_update_ws(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks, const KStage* kd,
+                      DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push);
 int update_tma_maps_per_block();
 void update_tma_box(int id, int box[3]);  // width, height, first cell rel. to the tile origin
 const double* update_tma_array(const DevBlock& B, int id);

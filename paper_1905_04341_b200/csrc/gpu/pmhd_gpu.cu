@@ -281,9 +281,12 @@ int build_update_maps(pmhd_mesh* m) {
 // kernel (default).
 void launch_update_any(pmhd_mesh* m, const KStage& ks, const KStage* kd, int want_dt, int kr0, int kr1,
                        cudaStream_t st, int push) {
+  const char* u = std::getenv("PMHD_UPDATE");  // (read per stage: tests switch it)
   if (m->upd_maps) {
     const CUtensorMap* maps = m->upd_maps + size_t(m->parity) * m->G.nb * update_tma_maps_per_block();
     launch_update_tma(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, maps, m->upd_xoff, push);
+  } else if (m->G.dim == 3 && u && std::string(u) == "ws") {
+    launch_update_ws(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, push);
   } else {
     launch_update_fused(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, m->ec_maps, push);
   }

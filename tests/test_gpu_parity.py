@@ -257,18 +257,20 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
         assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
 
 
+@pytest.mark.parametrize("alt", ["tma", "ws"])
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "wave3d_tiny_blocks", "wave3d_ng3_ragged",
                                   "wave3d_ng4_8blk", "turb3d", "blast3d_64_floor"])
-def test_update_kernels_bitwise(gpu_available, case, monkeypatch):
-    """The TMA-staged update kernel (3D, PMHD_UPDATE=tma) and the default LDG
-    update kernel compute the same expressions on the same operands: the
+def test_update_kernels_bitwise(gpu_available, case, alt, monkeypatch):
+    """The TMA-staged (PMHD_UPDATE=tma) and warp-specialised (PMHD_UPDATE=ws)
+    update kernels and the default LDG update kernel compute the same
+    expressions on the same operands: the
     parity build gives the same bits with either (the FMA build may contract
     a multiply-add differently in the two kernels; it is held to the oracle
     tolerance by test_fma_build_within_tolerance)."""
     kw, ncyc = CASES[case]
     cfg = RunConfig(**kw)
     out = []
-    for kern in ("ldg", "tma"):
+    for kern in ("ldg", alt):
         monkeypatch.setenv("PMHD_UPDATE", kern)
         g = GpuSolver(cfg, parity=True)
         g.load_pgen()

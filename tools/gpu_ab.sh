@@ -18,6 +18,8 @@ for v in "$@"; do
     slab*) PMHD_SLAB_PLANES=${v#slab} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     notma) PMHD_TMA=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     nooverlap) PMHD_OVERLAP=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    ws) PMHD_UPDATE=ws $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5ws) PMHD_UPDATE=ws $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     tma) PMHD_UPDATE=tma $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5tma) PMHD_UPDATE=tma $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     x1march) PMHD_FLUX_MARCH_X1=1 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
