@@ -46,6 +46,9 @@ constexpr int ECS = PMHD_UPDATE_TMA ? ((EX * EY * 8 + 127) / 128) * 16 : EX * EY
 // recomputed: the cell-centred E ring holds planes k and k+1 (one new plane
 // loaded per step), E1 / E2 at k+1/2 become the k-1/2 values of the next
 // step, and so does the new b3 face at k+1.
+#ifndef PMHD_UPD_EC_SMEM
+#define PMHD_UPD_EC_SMEM 1  // 0: read the cell-centred E through L1 instead of the shared-memory ring
+#endif
 #ifndef PMHD_UPD_FLAT_B
 #define PMHD_UPD_FLAT_B 0  // 1: phase B (E3 + E1 + E2) as one flat item list (spills at 48 regs: 1.79 vs 1.55 ms)
 #endif
@@ -68,7 +71,7 @@ __device__ __forceinline__ void ST(double* p, double v) {
 struct alignas(PMHD_UPDATE_TMA ? 128 : 16) UpdSmem {
   // cell-centred E ring: [component][k & 1] boxes of EY x EX (one TMA box
   // each; slots padded to 128 B multiples)
-  double ecbuf[3][2][ECS];
+  double ecbuf[3][2][PMHD_UPD_EC_SMEM ? ECS : 1];
   unsigned long long bar[2];    // TMA completion barriers, one per ring slot
   double e3s[UY + 1][UX + 1];   // E3 at (k, j-1/2, i-1/2)
   double e1s[2][UY + 1][UX];    // E1 at (k -/+ 1/2, j-1/2, i), slot by parity
@@ -100,6 +103,13 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
   UpdSmem& SM = *reinterpret_cast<UpdSmem*>(upd_smem);
 #endif
   auto ec = [&](int c, int sl) { return reinterpret_cast<double(*)[EX]>(&SM.ecbuf[c][sl][0]); };
+  // E of component c at E-box row r, column q of plane kk: the ring slot of
+  // kk, or (PMHD_UPD_EC_SMEM=0) straight from the array through L1
+  struct EcRows {
+    const double* p;
+    int sx;
+    __device__ __forceinline__ const double* operator[](int r) const { return p + r * sx; }
+  };
   auto& e3s = SM.e3s;
   auto& e1s = SM.e1s;
   auto& e2s = SM.e2s;
@@ -118,6 +128,11 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
   const int i0 = G.is + blockIdx.x * UX, j0 = G.js + blockIdx.y * UY;
   const int nx = min(UX, G.ie - i0), ny = min(UY, G.je - j0);
   const DevBlock& B = blks[b];
+#if PMHD_UPD_EC_SMEM
+  auto ecx = [&](int c, int kk) { return ec(c, kk & 1); };
+#else
+  auto ecx = [&](int c, int kk) { return EcRows{B.ec[c] + G.idx(kk, j0 - 1, i0 - 1), G.sx}; };
+#endif
   double* const* Sb = B.st[0];
   double* const* Sout = B.st[ks.out_sel];
   double* const* X1 = B.fx[0];
@@ -170,8 +185,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       double e;
       if (d3) {
         e = corner_emf(mode, X2[5][id], X2[5][id - sy], X3[6][id], X3[6][id - sx], X2[7][id],
-                       X2[7][id - sy], X3[7][id], X3[7][id - sx], ec(0, pa)[r + 1][c + 1],
-                       ec(0, pa)[r][c + 1], ec(0, pm)[r + 1][c + 1], ec(0, pm)[r][c + 1]);
+                       X2[7][id - sy], X3[7][id], X3[7][id - sx], ecx(0, kk)[r + 1][c + 1],
+                       ecx(0, kk)[r][c + 1], ecx(0, kk - 1)[r + 1][c + 1], ecx(0, kk - 1)[r][c + 1]);
       } else {
         e = X2[5][id];
       }
@@ -185,8 +200,8 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       double e;
       if (d3) {
         e = corner_emf(mode, X3[5][id], X3[5][id - 1], X1[6][id], X1[6][id - sy], X3[7][id],
-                       X3[7][id - 1], X1[7][id], X1[7][id - sy], ec(1, pa)[r + 1][c + 1],
-                       ec(1, pm)[r + 1][c + 1], ec(1, pa)[r + 1][c], ec(1, pm)[r + 1][c]);
+                       X3[7][id - 1], X1[7][id], X1[7][id - sy], ecx(1, kk)[r + 1][c + 1],
+                       ecx(1, kk - 1)[r + 1][c + 1], ecx(1, kk)[r + 1][c], ecx(1, kk - 1)[r + 1][c]);
       } else {
         e = X1[6][id];
       }
@@ -208,9 +223,9 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
         PMHD_CHECK_ID(G, id - G.sx);
         const int ec_c = c + 1, ec_r = r + 1;
         e3s[r][c] = corner_emf(mode, X1[5][id], X1[5][id - sx], X2[6][id], X2[6][id - 1], X1[7][id],
-                               X1[7][id - sx], X2[7][id], X2[7][id - 1], ec(2, lo)[ec_r][ec_c],
-                               ec(2, lo)[ec_r][ec_c - 1], ec(2, lo)[ec_r - 1][ec_c],
-                               ec(2, lo)[ec_r - 1][ec_c - 1]);
+                               X1[7][id - sx], X2[7][id], X2[7][id - 1], ecx(2, k)[ec_r][ec_c],
+                               ecx(2, k)[ec_r][ec_c - 1], ecx(2, k)[ec_r - 1][ec_c],
+                               ecx(2, k)[ec_r - 1][ec_c - 1]);
       } else if (q < NE3 + NE1) {
         const int q1 = q - NE3, c = q1 % UX, r = q1 / UX;
         if (c >= nx || r > ny) continue;
@@ -218,15 +233,15 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
         PMHD_CHECK_ID(G, id - G.sy);
         PMHD_CHECK_ID(G, id);
         e1s[hi][r][c] = corner_emf(mode, X2[5][id], X2[5][id - sy], X3[6][id], X3[6][id - sx], X2[7][id],
-                                   X2[7][id - sy], X3[7][id], X3[7][id - sx], ec(0, hi)[r + 1][c + 1],
-                                   ec(0, hi)[r][c + 1], ec(0, lo)[r + 1][c + 1], ec(0, lo)[r][c + 1]);
+                                   X2[7][id - sy], X3[7][id], X3[7][id - sx], ecx(0, kk)[r + 1][c + 1],
+                                   ecx(0, kk)[r][c + 1], ecx(0, k)[r + 1][c + 1], ecx(0, k)[r][c + 1]);
       } else {
         const int q2 = q - NE3 - NE1, c = q2 % (UX + 1), r = q2 / (UX + 1);
         if (c > nx || r >= ny) continue;
         const int id = G.idx(kk, j0 + r, i0 + c);
         e2s[hi][r][c] = corner_emf(mode, X3[5][id], X3[5][id - 1], X1[6][id], X1[6][id - sy], X3[7][id],
-                                   X3[7][id - 1], X1[7][id], X1[7][id - sy], ec(1, hi)[r + 1][c + 1],
-                                   ec(1, lo)[r + 1][c + 1], ec(1, hi)[r + 1][c], ec(1, lo)[r + 1][c]);
+                                   X3[7][id - 1], X1[7][id], X1[7][id - sy], ecx(1, kk)[r + 1][c + 1],
+                                   ecx(1, k)[r + 1][c + 1], ecx(1, kk)[r + 1][c], ecx(1, k)[r + 1][c]);
       }
     }
   };
@@ -282,8 +297,10 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
     wait_ec(kb - 1);
     wait_ec(kb);
   } else {
-    if (d3) load_ec(kb - 1);
-    load_ec(kb);
+    if (PMHD_UPD_EC_SMEM) {
+      if (d3) load_ec(kb - 1);
+      load_ec(kb);
+    }
   }
   __syncthreads();
   edge_emfs(kb, kb & 1);
@@ -297,7 +314,7 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
     if (PROF && tid == 0 && k > kb) { const long long t = clock64(); tph[2] += t - tph[0]; tph[0] = t; }
     // ---- A: the next Ec plane (slot of k-1, no longer needed) --------------
     if (tma) wait_ec(k + 1);
-    else if (d3) load_ec(k + 1);
+    else if (PMHD_UPD_EC_SMEM && d3) load_ec(k + 1);
     __syncthreads();
     // ---- B: E3 at plane k, E1 / E2 at k + 1/2 -------------------------------
     if (PMHD_UPD_FLAT_B && d3) emf_items(k, lo, hi);
@@ -310,9 +327,9 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
       PMHD_CHECK_ID(G, id - G.sx);
       const int ec_c = c + 1, ec_r = r + 1;
       e3s[r][c] = corner_emf(mode, X1[5][id], X1[5][id - sx], X2[6][id], X2[6][id - 1], X1[7][id],
-                             X1[7][id - sx], X2[7][id], X2[7][id - 1], ec(2, lo)[ec_r][ec_c],
-                             ec(2, lo)[ec_r][ec_c - 1], ec(2, lo)[ec_r - 1][ec_c],
-                             ec(2, lo)[ec_r - 1][ec_c - 1]);
+                             X1[7][id - sx], X2[7][id], X2[7][id - 1], ecx(2, k)[ec_r][ec_c],
+                             ecx(2, k)[ec_r][ec_c - 1], ecx(2, k)[ec_r - 1][ec_c],
+                             ecx(2, k)[ec_r - 1][ec_c - 1]);
     }
     edge_emfs(k + 1, hi);
     }
