@@ -422,7 +422,13 @@ def run_ours(args):
         "kernel": f"k_flux_fused (dominant: {flux_ms * n_flux / kern_ms:.0%} of the cycle; {n_flux} launches/cycle, "
                   f"avg {flux_ms:.3f} ms; F_alg(flux region) = {F_flux:.1f} flop/cell-update / {n_flux} launches)",
         "peak_source": fp64_src,
-        "note": "FP64 CUDA-core bound, neither HBM nor tensor cores: bound='fp64' against the measured DFMA peak",
+        "note": "FP64 CUDA-core bound, neither HBM nor tensor cores: bound='fp64' against the measured DFMA peak; "
+                "its load / store skeleton also moves ~2.4 GB per launch (hbm_view), DESIGN.md section 4a",
+        # the same kernel against the HBM ceiling: ncu DRAM bytes per launch
+        # over the event-timed launch duration
+        "hbm_view": ({"achieved": tr["flux_bytes_per_launch"] / (flux_ms * 1e-3) / 1e9, "peak": hbm_pk,
+                      "unit": "GB/s", "frac": tr["flux_bytes_per_launch"] / (flux_ms * 1e-3) / 1e9 / hbm_pk,
+                      "peak_source": hbm_src} if tr else None),
         "hbm_whole_cycle": {"achieved": ach_gbs, "peak": hbm_pk, "unit": "GB/s", "frac": ach_gbs / hbm_pk,
                             "B_alg_per_cell_update": B_ALG, "peak_source": hbm_src,
                             "ncu_dram_bytes_per_cell_update": tr["dram_bytes_per_cell_update"] if tr else None},
