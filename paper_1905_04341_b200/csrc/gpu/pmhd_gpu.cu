@@ -25,7 +25,7 @@
 using namespace pmhd_gpu;
 
 #ifndef PMHD_VARIANT
-#define PMHD_VARIANT "fused(flux x3 + update) [PMHD_KERNELS=split: one kernel per op]"
+#define PMHD_VARIANT "fused(flux: x1 tile, x2/x3 column march; update) [PMHD_KERNELS=split: one kernel per op]"
 #endif
 #ifdef PMHD_BOUNDS_CHECK
 #define PMHD_CHECK_INFO "+bounds-check"
