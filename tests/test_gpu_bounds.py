@@ -43,10 +43,22 @@ for name in names:
 """
 
 
+# the default kernel selection, then the round-2 alternatives forced on these
+# small meshes: column / row march flux kernels, the x1 + x2 kernel, and the
+# TMA-staged and warp-specialised update kernels
+VARIANTS = {
+    "default": {},
+    "march": {"PMHD_FLUX_MARCH": "2", "PMHD_FLUX_MARCH_X1": "1"},
+    "xy_tma": {"PMHD_FLUX_XY": "1", "PMHD_UPDATE": "tma"},
+    "march_ws": {"PMHD_FLUX_MARCH": "2", "PMHD_UPDATE": "ws"},
+}
+
+
 @pytest.mark.gpu
-def test_bounds_checked_build(gpu_available):
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_bounds_checked_build(gpu_available, variant):
     assert os.path.exists(LIB), "build it: make testlib"
-    env = dict(os.environ, PMHD_GPU_LIB=LIB)
+    env = dict(os.environ, PMHD_GPU_LIB=LIB, **VARIANTS[variant])
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], env=env, cwd=ROOT,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
