@@ -135,11 +135,19 @@ void launch_c2p_all(const DevBlock* blks, const KGeom& G, const KPhys& ph, int s
                     int stage, cudaStream_t s);
 void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel, int plm,
                  double c1024, cudaStream_t s);
+// Kernel choices of the flux launcher, read from the PMHD_* environment at
+// mesh creation (pmhd_gpu_mesh_create)
+struct FluxOpts {
+  int reuse = 0;     // owned-face ranges + rim images (PMHD_FACE_REUSE)
+  int march = 1;     // x2 / x3 column march: 0 off, 1 where it fills the GPU, 2 always (PMHD_FLUX_MARCH)
+  int march_x1 = 0;  // x1 row march (PMHD_FLUX_MARCH_X1, opt-in)
+  int pad = 0;       // experiment: unused dynamic shared memory per tile CTA, bytes (PMHD_FLUX_SMEM_PAD)
+};
 // region: 0 all tiles, 1 tiles clear of the ghost exchange, 2 the others
 // kd: nullptr (coefficients by value) or the device copy of a graph-replayed cycle
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
                        int plm, double c1024, const KStage* kd, int stage, DevRed* red, int slab,
-                       int nslab, int S, cudaStream_t s, int region = 0, int reuse = 0);
+                       int nslab, int S, cudaStream_t s, int region = 0, const FluxOpts& opt = FluxOpts());
 // x1 and x2 faces in one launch (owned-face ranges; kernels_flux.cu k_flux_xy)
 void launch_flux_xy(const DevBlock* blks, const KGeom& G, const KPhys& ph, int sel, int plm, double c1024x,
                     double c1024y, const KStage* kd, int stage, DevRed* red, cudaStream_t s);

@@ -1038,7 +1038,8 @@ k_flux_xy(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm
 // multiple of the x3 tile's FS (16).  nslab = 1 is the whole block.
 void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir, int sel,
                        int plm, double c1024, const KStage* kd, int stage, DevRed* red, int slab,
-                       int nslab, int S, cudaStream_t s, int region, int reuse) {
+                       int nslab, int S, cudaStream_t s, int region, const FluxOpts& opt) {
+  const int reuse = opt.reuse;
   const int d3 = (G.dim == 3) ? 1 : 0;
   // face ranges of the oracle: [lo, hi) per axis;
   // with owned-face reuse [s, e) on every axis (the rest are rim images)
@@ -1069,14 +1070,12 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   // kernel).  Measured at 256^3 per cycle: 7.56 ms against 7.73 for the tile
   // kernel with the next cell's raw values prefetched one step ahead; 7.80
   // without the prefetch (4 CTAs/SM), 7.93 at 5 CTAs/SM (spills)
-  // (read per launch: tests switch it; 2 forces the march on any mesh size)
-  const char* me = std::getenv("PMHD_FLUX_MARCH");
-  const int march_mode = me ? std::atoi(me) : 1;
+  // (PMHD_FLUX_MARCH=2 forces the march on any mesh size)
+  const int march_mode = opt.march;
   const bool march_on = march_mode != 0;
   // x1 faces: the row-march kernel with PMHD_FLUX_MARCH_X1=1 (measured at
   // 256^3: 7.574 ms per cycle against 7.566 for the x1 tile kernel)
-  const char* mx = std::getenv("PMHD_FLUX_MARCH_X1");
-  if (dir == 0 && march_on && mx && std::atoi(mx) != 0 && nslab == 1) {
+  if (dir == 0 && march_on && opt.march_x1 && nslab == 1) {
     const int nrow = (j1 - j0) * (k1 - k0);
     const dim3 xg((nrow + 3) / 4, G.nb, 1);
 #define PMHD_X1M_LAUNCH(R, M) \
@@ -1131,8 +1130,7 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   // experiment knob (PMHD_FLUX_SMEM_PAD = bytes of unused dynamic shared
   // memory per CTA): caps the flux CTAs per SM so that an update CTA of a
   // concurrent stream can co-reside (k-slab pipeline study)
-  int pad = 0;
-  if (const char* e = std::getenv("PMHD_FLUX_SMEM_PAD")) pad = std::max(0, std::atoi(e)) + (dir == 0 ? 1792 : 0);
+  const int pad = opt.pad ? opt.pad + (dir == 0 ? 1792 : 0) : 0;
 #define PMHD_FLUX_LAUNCH(D, R)                                                                      \
   do {                                                                                              \
     if (kd)                                                                                         \

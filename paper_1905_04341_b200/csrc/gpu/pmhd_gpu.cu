@@ -96,6 +96,9 @@ struct pmhd_mesh {
   int slab_planes = 0;            // k-slab pipeline depth (PMHD_SLAB_PLANES, 0 = off)
   bool push_x1 = false;           // update kernel writes the x1 ghosts (PMHD_PUSH_X1, default on when possible)
   bool face_reuse = false;        // flux tiles cover owned faces only + rim images (PMHD_FACE_REUSE)
+  FluxOpts fopt;                  // flux kernel choices (PMHD_FACE_REUSE / _FLUX_MARCH / _FLUX_MARCH_X1 / _FLUX_SMEM_PAD)
+  bool flux_xy = false;           // x1 + x2 in one launch (PMHD_FLUX_XY=1)
+  int upd_kind = 0;               // 3D update kernel: 0 LDG, 1 warp-specialised (PMHD_UPDATE=ws); tma: upd_maps
   std::vector<cudaEvent_t> slab_ev;
   cudaEvent_t ev[8] = {};
   cudaEvent_t xev[25] = {};        // host<->device transfer pipeline (one per staged array + 1)
@@ -281,11 +284,10 @@ int build_update_maps(pmhd_mesh* m) {
 // kernel (default).
 void launch_update_any(pmhd_mesh* m, const KStage& ks, const KStage* kd, int want_dt, int kr0, int kr1,
                        cudaStream_t st, int push) {
-  const char* u = std::getenv("PMHD_UPDATE");  // (read per stage: tests switch it)
   if (m->upd_maps) {
     const CUtensorMap* maps = m->upd_maps + size_t(m->parity) * m->G.nb * update_tma_maps_per_block();
     launch_update_tma(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, maps, m->upd_xoff, push);
-  } else if (m->G.dim == 3 && u && std::string(u) == "ws") {
+  } else if (m->G.dim == 3 && m->upd_kind == 1) {
     launch_update_ws(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, push);
   } else {
     launch_update_fused(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, m->ec_maps, push);
@@ -311,12 +313,10 @@ KStage make_stage(const KGeom& G, int s, double dt) {
 bool can_prefetch(const pmhd_mesh* m) { return m->overlap && m->variant == 0 && !m->prof; }
 
 // x1 and x2 faces in one k_flux_xy launch (PMHD_FLUX_XY=1): owned-face
-// ranges only (the two directions then share one tile grid); read per stage
-// (tests switch it)
+// ranges only (the two directions then share one tile grid)
 bool use_flux_xy(const pmhd_mesh* m) {
-  if (m->variant != 0 || !m->face_reuse) return false;
-  const char* e = std::getenv("PMHD_FLUX_XY");
-  return e && std::atoi(e) != 0;  // opt-in: measured 6.6 % slower at 256^3 (16 warps/SM)
+  // opt-in: measured 6.6 % slower at 256^3 (16 warps/SM)
+  return m->variant == 0 && m->face_reuse && m->flux_xy;
 }
 
 // Interior flux tiles of stage s on stream2, after the work already on the
@@ -330,7 +330,7 @@ int prefetch_stage(pmhd_mesh* m, int s, double dt) {
   CK(cudaStreamWaitEvent(ctx->stream2, m->ev_pre[0], 0));
   for (int dir = 0; dir < G.dim; ++dir)
     launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], nullptr, s, m->dred, 0,
-                      1, G.ke - G.ks, ctx->stream2, 1, m->face_reuse ? 1 : 0);
+                      1, G.ke - G.ks, ctx->stream2, 1, m->fopt);
   CK(cudaEventRecord(m->ev_pre[1], ctx->stream2));
   m->times.kernel_launches += G.dim;
   m->prefetched = s;
@@ -396,7 +396,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     for (int dir = xy ? 2 : 0; dir < G.dim; ++dir) {
       if (m->variant == 0)
         launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], kd, s, m->dred, 0, 1,
-                          nk, st, flux_region, m->face_reuse ? 1 : 0);
+                          nk, st, flux_region, m->fopt);
       else
         launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], st);
     }
@@ -748,6 +748,13 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   // k-slab pipeline (images cross slabs)
   m->face_reuse = m->all_local && m->slab_planes == 0;
   if (const char* fr = std::getenv("PMHD_FACE_REUSE")) m->face_reuse = m->face_reuse && std::atoi(fr) != 0;
+  // the other kernel choices, read once here
+  m->fopt.reuse = m->face_reuse ? 1 : 0;
+  if (const char* e = std::getenv("PMHD_FLUX_MARCH")) m->fopt.march = std::max(0, std::min(2, std::atoi(e)));
+  if (const char* e = std::getenv("PMHD_FLUX_MARCH_X1")) m->fopt.march_x1 = std::atoi(e) != 0 ? 1 : 0;
+  if (const char* e = std::getenv("PMHD_FLUX_SMEM_PAD")) m->fopt.pad = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("PMHD_FLUX_XY")) m->flux_xy = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PMHD_UPDATE")) m->upd_kind = (std::string(e) == "ws") ? 1 : 0;
   m->slab_ev.resize((G.ke - G.ks) / 8 + 2);
   for (auto& e : m->slab_ev) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   MCK(cudaStreamSynchronize(ctx->stream));
