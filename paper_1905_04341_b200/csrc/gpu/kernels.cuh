@@ -140,7 +140,11 @@ void launch_flux(const DevBlock* blks, const KGeom& G, const KPhys& ph, int dir,
 struct FluxOpts {
   int reuse = 0;     // owned-face ranges + rim images (PMHD_FACE_REUSE)
   int march = 1;     // x2 / x3 column march: 0 off, 1 where it fills the GPU, 2 always (PMHD_FLUX_MARCH)
-  int march_x1 = 0;  // x1 row march (PMHD_FLUX_MARCH_X1, opt-in)
+  int march_x1 = 1;  // x1 row march too (PMHD_FLUX_MARCH_X1)
+  // bit s-1: the march kernels in stage s (PMHD_FLUX_MARCH_STAGES): stage 2
+  // only -- with donor-cell states (stage 1) the tile kernels are as fast or
+  // faster, with PLM (stage 2) the marches win
+  int march_stages = 2;
   int pad = 0;       // experiment: unused dynamic shared memory per tile CTA, bytes (PMHD_FLUX_SMEM_PAD)
 };
 // region: 0 all tiles, 1 tiles clear of the ghost exchange, 2 the others

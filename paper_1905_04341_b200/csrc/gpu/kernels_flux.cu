@@ -1072,12 +1072,15 @@ void launch_flux_fused(const DevBlock* blks, const KGeom& G, const KPhys& ph, in
   // without the prefetch (4 CTAs/SM), 7.93 at 5 CTAs/SM (spills)
   // (PMHD_FLUX_MARCH=2 forces the march on any mesh size)
   const int march_mode = opt.march;
-  const bool march_on = march_mode != 0;
-  // x1 faces: the row-march kernel with PMHD_FLUX_MARCH_X1=1 (measured at
-  // 256^3: 7.574 ms per cycle against 7.566 for the x1 tile kernel)
-  if (dir == 0 && march_on && opt.march_x1 && nslab == 1) {
-    const int nrow = (j1 - j0) * (k1 - k0);
-    const dim3 xg((nrow + 3) / 4, G.nb, 1);
+  const bool march_on = march_mode != 0 && ((opt.march_stages >> (plm ? 1 : 0)) & 1);
+  // x1 faces: the row-march kernel (stage 2 by default; PMHD_FLUX_MARCH_X1=0:
+  // the x1 tile kernel).  Measured at 256^3 per cycle with the marches in
+  // stage 2 only: 7.45-7.47 ms with the x1 row march, 7.53 without; in both
+  // stages 7.57-7.60 either way
+  const int nrow = (j1 - j0) * (k1 - k0);
+  const dim3 xg((nrow + 3) / 4, G.nb, 1);
+  const bool x1_fills = march_mode == 2 || (long long)xg.x * xg.y >= 2LL * 148 * PMHD_MARCH_MINB;
+  if (dir == 0 && march_on && opt.march_x1 && x1_fills && nslab == 1) {
 #define PMHD_X1M_LAUNCH(R, M) \
   k_flux_x1march<R, M><<<xg, XT, 0, s>>>(blks, G, ph, sel, plm, c1024, kd, stage, red, i0, i1, j0, j1, k0, k1, \
                                          region, reuse)

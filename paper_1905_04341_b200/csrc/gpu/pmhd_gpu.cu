@@ -752,6 +752,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   m->fopt.reuse = m->face_reuse ? 1 : 0;
   if (const char* e = std::getenv("PMHD_FLUX_MARCH")) m->fopt.march = std::max(0, std::min(2, std::atoi(e)));
   if (const char* e = std::getenv("PMHD_FLUX_MARCH_X1")) m->fopt.march_x1 = std::atoi(e) != 0 ? 1 : 0;
+  if (const char* e = std::getenv("PMHD_FLUX_MARCH_STAGES")) m->fopt.march_stages = std::atoi(e) & 3;
   if (const char* e = std::getenv("PMHD_FLUX_SMEM_PAD")) m->fopt.pad = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("PMHD_FLUX_XY")) m->flux_xy = std::atoi(e) != 0;
   if (const char* e = std::getenv("PMHD_UPDATE")) m->upd_kind = (std::string(e) == "ws") ? 1 : 0;

@@ -48,9 +48,9 @@ for name in names:
 # TMA-staged and warp-specialised update kernels
 VARIANTS = {
     "default": {},
-    "march": {"PMHD_FLUX_MARCH": "2", "PMHD_FLUX_MARCH_X1": "1"},
+    "march": {"PMHD_FLUX_MARCH": "2", "PMHD_FLUX_MARCH_X1": "1", "PMHD_FLUX_MARCH_STAGES": "3"},
     "xy_tma": {"PMHD_FLUX_XY": "1", "PMHD_UPDATE": "tma"},
-    "march_ws": {"PMHD_FLUX_MARCH": "2", "PMHD_UPDATE": "ws"},
+    "march_ws": {"PMHD_FLUX_MARCH": "2", "PMHD_FLUX_MARCH_STAGES": "3", "PMHD_UPDATE": "ws"},
 }
 
 

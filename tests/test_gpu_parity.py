@@ -317,14 +317,15 @@ def test_flux_xy_bitwise(gpu_available, case, monkeypatch):
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_ragged", "wave3d_tiny_blocks",
                                   "wave3d_ng3_ragged", "wave3d_roe", "wave3d_hlle_vl_arith"])
 def test_flux_kernels_bitwise(gpu_available, case, reuse, monkeypatch):
-    """The column-march x2 / x3 flux kernel (default) with the row-march x1
-    kernel (opt-in) and the tile kernels (PMHD_FLUX_MARCH=0) give the same
-    bits in the parity build, with the
+    """The column-march x2 / x3 and row-march x1 flux kernels (the stage-2
+    default; forced here in both stages) and the tile kernels
+    (PMHD_FLUX_MARCH=0) give the same bits in the parity build, with the
     owned-face ranges and with the extended ones."""
     kw, ncyc = CASES[case]
     cfg = RunConfig(**kw)
     monkeypatch.setenv("PMHD_FACE_REUSE", reuse)
-    monkeypatch.setenv("PMHD_FLUX_MARCH_X1", "1")  # the x1 row march too (opt-in)
+    monkeypatch.setenv("PMHD_FLUX_MARCH_X1", "1")  # the x1 row march too
+    monkeypatch.setenv("PMHD_FLUX_MARCH_STAGES", "3")  # in both stages (default: stage 2)
     out = []
     for march in ("0", "2"):  # 2: the march kernels even on these small meshes
         monkeypatch.setenv("PMHD_FLUX_MARCH", march)
@@ -377,6 +378,7 @@ def test_overlap_prefetch_bitwise(gpu_available, case, march, monkeypatch):
     column-march x2 / x3 kernels (their region split) on these small meshes."""
     monkeypatch.setenv("PMHD_OVERLAP", "1")
     monkeypatch.setenv("PMHD_FLUX_MARCH", march)
+    monkeypatch.setenv("PMHD_FLUX_MARCH_STAGES", "3")
     kw, ncyc = CASES[case]
     cfg = RunConfig(**kw)
     o, g, _, (fo, fg), dts = run_pair(cfg, ncyc, parity=True)
@@ -441,6 +443,7 @@ def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered, case
     interior / boundary split (the halo overlap) is covered too."""
     from paper_1905_04341_b200.parallel import plan_for, LoopbackWorld
     monkeypatch.setenv("PMHD_FLUX_MARCH", march)
+    monkeypatch.setenv("PMHD_FLUX_MARCH_STAGES", "3")
     cfg = RunConfig(**MULTIRANK[case])
     plan = plan_for(cfg, nranks)
     engines = [GpuSolver(cfg, parity=True, gids=plan.local_gids(r)) for r in range(nranks)]

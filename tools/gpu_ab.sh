@@ -22,8 +22,13 @@ for v in "$@"; do
     m5ws) PMHD_UPDATE=ws $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     tma) PMHD_UPDATE=tma $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5tma) PMHD_UPDATE=tma $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    nox1march) PMHD_FLUX_MARCH_X1=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    both) PMHD_FLUX_MARCH_STAGES=3 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     x1march) PMHD_FLUX_MARCH_X1=1 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5x1march) PMHD_FLUX_MARCH_X1=1 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    st2) PMHD_FLUX_MARCH_STAGES=2 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    st2x1) PMHD_FLUX_MARCH_STAGES=2 PMHD_FLUX_MARCH_X1=1 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5st2x1) PMHD_FLUX_MARCH_STAGES=2 PMHD_FLUX_MARCH_X1=1 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     tile) PMHD_FLUX_MARCH=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5tile) PMHD_FLUX_MARCH=0 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     noreuse) PMHD_FACE_REUSE=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
