@@ -25,7 +25,8 @@
 using namespace pmhd_gpu;
 
 #ifndef PMHD_VARIANT
-#define PMHD_VARIANT "fused(flux: x1 tile, x2/x3 column march; update) [PMHD_KERNELS=split: one kernel per op]"
+// (no commas: the string is the policy column of the CLI's CSV row)
+#define PMHD_VARIANT "fused(flux: tile + march; update) [PMHD_KERNELS=split: one kernel per op]"
 #endif
 #ifdef PMHD_BOUNDS_CHECK
 #define PMHD_CHECK_INFO "+bounds-check"
