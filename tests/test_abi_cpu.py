@@ -29,6 +29,17 @@ def test_gpu_library_exports_header(parity):
     assert set(names) == set(N.GPU_SYMBOLS)
 
 
+@pytest.mark.parametrize("parity", [False, True])
+def test_build_info_is_one_csv_field(parity):
+    """pmhd_gpu_build_info() (host-only, no device needed) is the policy
+    column of `pmhd bench`'s CSV row: no commas or newlines."""
+    lib = ctypes.CDLL(str(N.gpu_lib_path(parity)), mode=ctypes.RTLD_LOCAL)
+    lib.pmhd_gpu_build_info.restype = ctypes.c_char_p
+    info = lib.pmhd_gpu_build_info().decode()
+    assert info and "," not in info and "\n" not in info, info
+    assert info.endswith("+parity(fmad=false)") == parity
+
+
 def test_gpu_library_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", str(N.gpu_lib_path(False))],
