@@ -419,7 +419,7 @@ def run_ours(args):
         "bound": "fp64", "achieved": flux_tf, "peak": fp64_pk, "unit": "TFLOP/s",
         "frac": flux_tf / fp64_pk,
         "traffic": tr["flux_bytes_per_launch"] if tr else None,
-        "kernel": f"flux kernels (k_flux_fused x1, k_flux_march x2/x3 on meshes that fill the GPU; dominant: {flux_ms * n_flux / kern_ms:.0%} of the cycle; {n_flux} launches/cycle, "
+        "kernel": f"flux kernels (stage 1: k_flux_fused tiles; stage 2: k_flux_x1march, k_flux_march on meshes that fill the GPU; dominant: {flux_ms * n_flux / kern_ms:.0%} of the cycle; {n_flux} launches/cycle, "
                   f"avg {flux_ms:.3f} ms; F_alg(flux region) = {F_flux:.1f} flop/cell-update / {n_flux} launches)",
         "peak_source": fp64_src,
         "note": "FP64 CUDA-core bound, neither HBM nor tensor cores: bound='fp64' against the measured DFMA peak; "

@@ -16,7 +16,7 @@ for row in r:
     d = dict(zip(h, row))
     b = val(d, "dram__bytes_read.sum") + val(d, "dram__bytes_write.sum")
     name = d["Kernel Name"]
-    (flux if ("k_flux_fused" in name or "k_flux_march" in name) else upd if "k_update_fused" in name else []).append(b)
+    (flux if ("k_flux_fused" in name or "k_flux_march" in name or "k_flux_x1march" in name) else upd if "k_update_fused" in name else []).append(b)
 res = {"report": rep, "active_cells": cells, "flux_launches": len(flux), "update_launches": len(upd),
        "flux_bytes_per_launch": sum(flux) / max(1, len(flux)),
        "update_bytes_per_launch": sum(upd) / max(1, len(upd)),
