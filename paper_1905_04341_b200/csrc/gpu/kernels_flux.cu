@@ -939,24 +939,30 @@ k_flux_xy(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int plm
     for (int v = 0; v < 8; ++v) P[v * XY_NCELL + c] = w[v];
   };
   constexpr int PER = (XY_NCELL + XY_T - 1) / XY_T;
+  // all of this thread's cells' raw values in flight before any is converted
+  double ub[PER][11];
+  int cid[PER];
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
     const int c = tid + p * XY_T;
     int i, j;
+    cid[p] = -1;
     if (!cell_ij(c, i, j)) continue;
     const int id = G.idx(k, j, i);
     PMHD_CHECK_ID(G, id + G.sy);
-    double ub[11];
+    cid[p] = id;
 #pragma unroll
-    for (int v = 0; v < 5; ++v) ub[v] = __ldg(S[v] + id);
-    ub[5] = __ldg(S[5] + id);
-    ub[6] = __ldg(S[5] + id + 1);
-    ub[7] = __ldg(S[6] + id);
-    ub[8] = __ldg(S[6] + id + G.sx);
-    ub[9] = __ldg(S[7] + id);
-    ub[10] = __ldg(S[7] + id + G.sy);
-    finish(c, id, ub);
+    for (int v = 0; v < 5; ++v) ub[p][v] = __ldg(S[v] + id);
+    ub[p][5] = __ldg(S[5] + id);
+    ub[p][6] = __ldg(S[5] + id + 1);
+    ub[p][7] = __ldg(S[6] + id);
+    ub[p][8] = __ldg(S[6] + id + G.sx);
+    ub[p][9] = __ldg(S[7] + id);
+    ub[p][10] = __ldg(S[7] + id + G.sy);
   }
+#pragma unroll
+  for (int p = 0; p < PER; ++p)
+    if (cid[p] >= 0) finish(tid + p * XY_T, cid[p], ub[p]);
   __syncthreads();
   if (PROF && tid == 0) tph[1] = clock64();
   long long trec = 0, trie = 0;
@@ -1164,16 +1170,17 @@ void launch_flux_xy(const DevBlock* blks, const KGeom& G, const KPhys& ph, int s
                     double c1024y, const KStage* kd, int stage, DevRed* red, cudaStream_t s) {
   const int write_ec = (G.dim == 2) ? 1 : 0;
   const dim3 grid((G.ie - G.is + XY_FX - 1) / XY_FX, (G.je - G.js + XY_FY - 1) / XY_FY, (G.ke - G.ks) * G.nb);
-  constexpr int smem = (8 * XY_NCELL + 14 * XY_RS) * 8;
+  constexpr int smem_max = (8 * XY_NCELL + 14 * XY_RS) * 8;
+  const int smem = plm ? smem_max : 8 * XY_NCELL * 8;  // donor cell: no reconstruction buffer
 #define PMHD_XY_LAUNCH(R)                                                                               \
   do {                                                                                                  \
     static std::atomic<unsigned long long> attr_devs{0};                                                \
     int dev = 0;                                                                                        \
     cudaGetDevice(&dev);                                                                                \
     if (!(attr_devs.load() & (1ULL << (dev & 63)))) {                                                   \
-      cudaFuncSetAttribute(k_flux_xy<R, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
-      cudaFuncSetAttribute(k_flux_xy<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
-      cudaFuncSetAttribute(k_flux_xy<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
+      cudaFuncSetAttribute(k_flux_xy<R, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);     \
+      cudaFuncSetAttribute(k_flux_xy<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);     \
+      cudaFuncSetAttribute(k_flux_xy<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);     \
       attr_devs.fetch_or(1ULL << (dev & 63));                                                           \
     }                                                                                                   \
     if (kd) k_flux_xy<R, 2><<<grid, XY_T, smem, s>>>(blks, G, ph, sel, plm, c1024x, c1024y, kd, stage, red, write_ec); \

@@ -98,7 +98,7 @@ struct pmhd_mesh {
   bool push_x1 = false;           // update kernel writes the x1 ghosts (PMHD_PUSH_X1, default on when possible)
   bool face_reuse = false;        // flux tiles cover owned faces only + rim images (PMHD_FACE_REUSE)
   FluxOpts fopt;                  // flux kernel choices (PMHD_FACE_REUSE / _FLUX_MARCH / _FLUX_MARCH_X1 / _FLUX_SMEM_PAD)
-  bool flux_xy = false;           // x1 + x2 in one launch (PMHD_FLUX_XY=1)
+  int flux_xy = 0;                // x1 + x2 in one launch, bit s-1 for stage s (PMHD_FLUX_XY=1|2|3)
   int upd_kind = 0;               // 3D update kernel: 0 LDG, 1 warp-specialised (PMHD_UPDATE=ws); tma: upd_maps
   std::vector<cudaEvent_t> slab_ev;
   cudaEvent_t ev[8] = {};
@@ -315,9 +315,10 @@ bool can_prefetch(const pmhd_mesh* m) { return m->overlap && m->variant == 0 && 
 
 // x1 and x2 faces in one k_flux_xy launch (PMHD_FLUX_XY=1): owned-face
 // ranges only (the two directions then share one tile grid)
-bool use_flux_xy(const pmhd_mesh* m) {
-  // opt-in: measured 6.6 % slower at 256^3 (16 warps/SM)
-  return m->variant == 0 && m->face_reuse && m->flux_xy;
+bool use_flux_xy(const pmhd_mesh* m, int s) {
+  // opt-in: measured 6.6 % slower at 256^3 in both stages (16 warps/SM);
+  // PMHD_FLUX_XY=1: both stages, 2: stage 1 only (bit 0), 3: both
+  return m->variant == 0 && m->face_reuse && ((m->flux_xy >> (s - 1)) & 1);
 }
 
 // Interior flux tiles of stage s on stream2, after the work already on the
@@ -392,7 +393,7 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     rec(m, 0);
     if (m->variant == 1) launch_c2p_all(m->dblk, G, m->ph, ks.in_sel, m->dred, s, st);
     rec(m, 1);
-    const bool xy = use_flux_xy(m) && flux_region == 0;
+    const bool xy = use_flux_xy(m, s) && flux_region == 0;
     if (xy) launch_flux_xy(m->dblk, G, m->ph, ks.in_sel, ks.plm, ks.c1024[0], ks.c1024[1], kd, s, m->dred, st);
     for (int dir = xy ? 2 : 0; dir < G.dim; ++dir) {
       if (m->variant == 0)
@@ -755,7 +756,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   if (const char* e = std::getenv("PMHD_FLUX_MARCH_X1")) m->fopt.march_x1 = std::atoi(e) != 0 ? 1 : 0;
   if (const char* e = std::getenv("PMHD_FLUX_MARCH_STAGES")) m->fopt.march_stages = std::atoi(e) & 3;
   if (const char* e = std::getenv("PMHD_FLUX_SMEM_PAD")) m->fopt.pad = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("PMHD_FLUX_XY")) m->flux_xy = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PMHD_FLUX_XY")) m->flux_xy = (std::atoi(e) == 1) ? 3 : (std::atoi(e) & 3);
   if (const char* e = std::getenv("PMHD_UPDATE")) m->upd_kind = (std::string(e) == "ws") ? 1 : 0;
   m->slab_ev.resize((G.ke - G.ks) / 8 + 2);
   for (auto& e : m->slab_ev) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1018,7 +1019,8 @@ int graph_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int
   // cycles that ran: the completed ones, plus the failing one (its stages ran
   // and flipped the tables inside the graph)
   const int ran = c.cycles + (c.err_key != ULLONG_MAX ? 1 : 0);
-  const long long per_cycle = 2 + 2 * (2 * G.dim + 1 - (m->push_x1 ? 1 : 0) - (use_flux_xy(m) ? 1 : 0));
+  const long long per_cycle = 2 * (2 * G.dim + 1 - (m->push_x1 ? 1 : 0)) + 2 - (use_flux_xy(m, 1) ? 1 : 0) -
+                              (use_flux_xy(m, 2) ? 1 : 0);
   m->times.kernel_launches += per_cycle * ran;
   if (ran & 1) {  // the state is in the other table after an odd number of cycles
     std::swap(m->hblk, m->hblk_alt);

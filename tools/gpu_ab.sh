@@ -10,6 +10,8 @@ for v in "$@"; do
     default) $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     ovlpad*) PMHD_FACE_REUSE=0 PMHD_SLAB_PLANES=${v#ovlpad} PMHD_FLUX_SMEM_PAD=11776 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     ovlnr*) PMHD_FACE_REUSE=0 PMHD_SLAB_PLANES=${v#ovlnr} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    xy1) PMHD_FLUX_XY=2 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5xy1) PMHD_FLUX_XY=2 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     xy) PMHD_FLUX_XY=1 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5xy) PMHD_FLUX_XY=1 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     padonly) PMHD_FLUX_SMEM_PAD=11776 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
