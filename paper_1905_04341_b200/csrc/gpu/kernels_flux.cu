@@ -602,11 +602,21 @@ k_flux_march(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, int sel, int 
   const int ahead = plm ? 1 : 0;  // step f converts cell f + ahead
   double pre[11];
   if (PMHD_MARCH_PREFETCH) load_raw(m0 + ahead, pre);
+#if PMHD_MARCH_PREFETCH == 2
+  double pre2[11];  // two cells ahead
+  if (m0 + 1 < m1) load_raw(m0 + 1 + ahead, pre2);
+#endif
   for (int f = m0; f < m1; ++f) {
     // cell f (donor) / f+1 (PLM) -- the last one the face at f needs
     if (PMHD_MARCH_PREFETCH) {
       conv(f + ahead, slot(f + ahead), pre);
+#if PMHD_MARCH_PREFETCH == 2
+#pragma unroll
+      for (int q = 0; q < 11; ++q) pre[q] = pre2[q];
+      if (f + 2 < m1) load_raw(f + 2 + ahead, pre2);
+#else
       if (f + 1 < m1) load_raw(f + 1 + ahead, pre);
+#endif
     } else {
       cell(f + ahead, slot(f + ahead));
     }
