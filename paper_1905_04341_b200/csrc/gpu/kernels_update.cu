@@ -444,8 +444,14 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
         double u[5];
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
+#if PMHD_DIAG_UPD_DU == 1  // diagnostic (never shipped): one flux load per direction
+          double du = 1e-30 * (c1 * X1[v][id] + c2 * X2[v][id] + c3 * X3[v][id]);
+#elif PMHD_DIAG_UPD_DU == 2  // diagnostic: no flux loads
+          double du = 0.0;
+#else
           double du = c1 * (X1[v][id + 1] - X1[v][id]) + c2 * (X2[v][id + sx] - X2[v][id]);
           if (d3) du = du + c3 * (X3[v][id + sy] - X3[v][id]);
+#endif
           u[v] = Sb[v][id] - du;
         }
         double bc[3], w[8];

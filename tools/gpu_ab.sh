@@ -51,7 +51,7 @@ v=sys.argv[1]
 try:
     d=json.load(open(f"gpurun_out/ab_{v}.json"))
     r=d["roofline"]
-    print(f"{v:10s} cups={d['value']:.4g} ms/step={d['ms_per_step']:.3f} flux_fp64={r['frac']:.3f} cyc_fp64={r['fp64_whole_cycle']['frac']:.3f} shares={ {k:round(x,3) for k,x in r['region_share'].items()} } clk={d['clocks']}")
+    print(f"{v:10s} cups={d['value']:.4g} ms/step={d['ms_per_step']:.3f} flux_ms={r['kernel'].split('avg ')[1].split(' ms')[0]} upd_ms={r['update_kernel']['avg_ms']:.3f} flux_fp64={r['frac']:.3f} cyc_fp64={r['fp64_whole_cycle']['frac']:.3f} shares={ {k:round(x,3) for k,x in r['region_share'].items()} } clk={d['clocks']}")
 except Exception as e:
     print(v, "FAILED", e, open(f"gpurun_out/ab_{v}.err").read()[-500:])
 PY
