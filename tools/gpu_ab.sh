@@ -7,6 +7,9 @@ B="python bench.py --steps 6 --warmup 3 --no-cpu-baseline --no-e2e"
 for v in "$@"; do
   case $v in
     split) PMHD_KERNELS=split $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    conc*) PMHD_FLUX_CONC=${v#conc} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5conc*) PMHD_FLUX_CONC=${v#m5conc} $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    b128conc*) PMHD_FLUX_CONC=${v#b128conc} $B --block 128 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     default) $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     ovlpad*) PMHD_FACE_REUSE=0 PMHD_SLAB_PLANES=${v#ovlpad} PMHD_FLUX_SMEM_PAD=11776 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     ovlnr*) PMHD_FACE_REUSE=0 PMHD_SLAB_PLANES=${v#ovlnr} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
