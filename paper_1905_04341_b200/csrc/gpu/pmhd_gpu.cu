@@ -403,7 +403,8 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     if (xy) launch_flux_xy(m->dblk, G, m->ph, ks.in_sel, ks.plm, ks.c1024[0], ks.c1024[1], kd, s, m->dred, st);
     // concurrent flux launches (PMHD_FLUX_CONC, opt-in): one direction on
     // stream2 beside the other two on the main stream, joined before the update
-    const int cdir = (m->flux_conc && m->variant == 0 && flux_region == 0 && !xy && !m->prof && G.dim == 3)
+    const int cdir = (m->flux_conc && m->variant == 0 && flux_region == 0 && !xy && !m->prof &&
+                      (G.dim == 3 || (G.dim == 2 && m->flux_conc == 1)))
                          ? m->flux_conc : -1;
     // stream of each direction's flux launch
     cudaStream_t fst[3] = {st, st, st};
