@@ -308,7 +308,11 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
   if (tma && kb + 1 <= kend) issue_ec(kb + 1);  // (slot of kb-1, read by the edge EMFs above)
   face_b3(kb, kb & 1);
 
+#ifdef PMHD_DIAG_UPD_NO_D
+  double tmin = 1.0e-5;
+#else
   double tmin = 1.0e300;
+#endif
   for (int k = kb; k < kend; ++k) {
     const int lo = k & 1, hi = lo ^ 1;  // slots of k - 1/2 and k + 1/2
     if (PROF && tid == 0 && k > kb) { const long long t = clock64(); tph[2] += t - tph[0]; tph[0] = t; }
@@ -437,7 +441,16 @@ k_update_fused(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_a
     // ---- D: conserved update + end-of-stage cons_to_prim + dt --------------
     {
       const int c = tid % UX, r = tid / UX;
+#ifdef PMHD_DIAG_UPD_NO_D  // diagnostic (never shipped): EMF + CT phases + a state copy only
       if (c < nx && r < ny) {
+        const int id = G.idx(k, j0 + r, i0 + c);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) ST(Sout[v] + id, Sb[v][id]);
+      }
+      if (false) {
+#else
+      if (c < nx && r < ny) {
+#endif
         const int i = i0 + c, j = j0 + r;
         const int id = G.idx(k, j, i);
         PMHD_CHECK_ID(G, id + G.sy);
