@@ -369,6 +369,33 @@ def test_face_reuse_bitwise(gpu_available, case, monkeypatch):
             assert np.array_equal(getattr(b0, f), getattr(b1, f)), (case, f)
 
 
+@pytest.mark.parametrize("conc", ["2", "3"])
+@pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_ragged", "turb3d"])
+def test_flux_streams_bitwise(gpu_available, case, conc, monkeypatch):
+    """Flux launches of a stage on two or three streams (PMHD_FLUX_CONC; 1,
+    x2 beside x1 -> x3, is the default) give the serial order's results bit
+    for bit in the product build: the launches write disjoint arrays and the
+    update waits for all of them."""
+    kw, ncyc = CASES[case]
+    cfg = RunConfig(**kw)
+    out = []
+    for c in ("0", "1", conc):
+        monkeypatch.setenv("PMHD_FLUX_CONC", c)
+        g = GpuSolver(cfg)
+        g.load_pgen()
+        dt = g.new_dt()
+        dts = []
+        for _ in range(ncyc):
+            dt, _st = g.vl2_step(dt)
+            dts.append(dt)
+        out.append((dts, [g.get_block(gid) for gid in range(cfg.nblocks)]))
+    for o in out[1:]:
+        assert o[0] == out[0][0]
+        for b0, b1 in zip(out[0][1], o[1]):
+            for f in ("u", "b1f", "b2f", "b3f"):
+                assert np.array_equal(getattr(b0, f), getattr(b1, f)), (case, f)
+
+
 @pytest.mark.parametrize("march", ["1", "2"])
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_4blk"])
 def test_overlap_prefetch_bitwise(gpu_available, case, march, monkeypatch):
