@@ -13,7 +13,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -Xlinker -Bsymbolic -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Iinclude -I$(GPUSRC) \
             -Xptxas -warn-spills --expt-relaxed-constexpr
 HOSTFLAGS:= -std=c++20 -O2 -march=x86-64-v3 -fPIC -Wall -Wextra -Iinclude
-GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu $(GPUSRC)/kernels_flux.cu $(GPUSRC)/kernels_update.cu $(GPUSRC)/kernels_update_tma.cu $(GPUSRC)/kernels_update_ws.cu $(GPUSRC)/kernels_halo.cu $(GPUSRC)/kernels_drive.cu $(GPUSRC)/kernels_ctl.cu
+GPU_SRCS := $(GPUSRC)/pmhd_gpu.cu $(GPUSRC)/kernels_split.cu $(GPUSRC)/kernels_flux.cu $(GPUSRC)/kernels_update.cu $(GPUSRC)/kernels_update_tma.cu $(GPUSRC)/kernels_update_ws.cu $(GPUSRC)/kernels_update_emf.cu $(GPUSRC)/kernels_halo.cu $(GPUSRC)/kernels_drive.cu $(GPUSRC)/kernels_ctl.cu
 # product division / sqrt: MUFU seed + one cubic Newton step, within 1 ulp
 # (tests/test_divsqrt.py); -DPMHD_FAST_DIVSQRT alone is the IEEE-exact variant
 FASTDS   := -DPMHD_FAST_DIVSQRT -DPMHD_DIVSQRT_1ULP

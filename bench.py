@@ -414,7 +414,12 @@ def run_ours(args):
     flux_tf = flux_flops / (flux_ms * 1e-3) / 1e12
     tr = (ncu_traffic() if args.workload == "m4" and args.size == 256 and dim == 3 and args.block in (0, 256)
           else None)
-    upd_ms = (rte["ct_emf_ms"] + rte["integrate_ms"]) / nprof / 2  # update kernel (events pass)
+    upd_ms = (rte["ct_emf_ms"] + rte["integrate_ms"]) / nprof / 2  # update kernel(s) per stage (events pass)
+    # 3D meshes that fill the GPU run the stage's update as two kernels
+    # (PMHD_UPDATE unset or "emf"); "ldg" / smaller meshes: the fused kernel
+    upd_env = os.environ.get("PMHD_UPDATE", "")
+    upd_name = ("k_edge_emf + k_cell_update (per stage)" if upd_env in ("", "emf") and cfg.desc.nx[2] > 1
+                else {"ws": "k_update_ws", "tma": "k_update_tma"}.get(upd_env, "k_update_fused"))
     roofline = {
         "bound": "fp64", "achieved": flux_tf, "peak": fp64_pk, "unit": "TFLOP/s",
         "frac": flux_tf / fp64_pk,
@@ -434,7 +439,7 @@ def run_ours(args):
                             "ncu_dram_bytes_per_cell_update": tr["dram_bytes_per_cell_update"] if tr else None},
         "fp64_whole_cycle": {"achieved": ach_tf, "peak": fp64_pk, "unit": "TFLOP/s", "frac": ach_tf / fp64_pk,
                              "F_alg_per_cell_update": F_alg, "F_alg_source": F_src},
-        "update_kernel": {"name": "k_update_fused", "avg_ms": upd_ms,
+        "update_kernel": {"name": upd_name, "avg_ms": upd_ms,
                           "dram_bytes_per_launch": tr["update_bytes_per_launch"] if tr else None,
                           "dram_gbs": (tr["update_bytes_per_launch"] / (upd_ms * 1e-3) / 1e9) if tr else None},
         "binding_ceiling": "fp64" if F_alg / fp64_pk > B_ALG / (hbm_pk / 1e3) else "hbm",

@@ -26,7 +26,7 @@ using namespace pmhd_gpu;
 
 #ifndef PMHD_VARIANT
 // (no commas: the string is the policy column of the CLI's CSV row)
-#define PMHD_VARIANT "fused(flux: tile + march; update) [PMHD_KERNELS=split: one kernel per op]"
+#define PMHD_VARIANT "fused(flux: tile + march; update: edge EMF + cell) [PMHD_KERNELS=split: one kernel per op]"
 #endif
 #ifdef PMHD_BOUNDS_CHECK
 #define PMHD_CHECK_INFO "+bounds-check"
@@ -105,7 +105,10 @@ struct pmhd_mesh {
   // (+0.6-0.8 % at 256^3). PMHD_FLUX_CONC: 0 off, 1 x2 (default), 2 x3, 3 x2 and x3
   int flux_conc = 1;
   cudaEvent_t ev_fx[3] = {};
-  int upd_kind = 0;               // 3D update kernel: 0 LDG, 1 warp-specialised (PMHD_UPDATE=ws); tma: upd_maps
+  // 3D update: 2 two kernels (edge EMFs + cell update) where they fill the
+  // GPU, else the fused LDG kernel (default); 0 fused (PMHD_UPDATE=ldg), 1
+  // warp-specialised (=ws), 3 two kernels always (=emf); tma: upd_maps
+  int upd_kind = 2;
   std::vector<cudaEvent_t> slab_ev;
   cudaEvent_t ev[8] = {};
   cudaEvent_t xev[25] = {};        // host<->device transfer pipeline (one per staged array + 1)
@@ -294,6 +297,11 @@ void launch_update_any(pmhd_mesh* m, const KStage& ks, const KStage* kd, int wan
   if (m->upd_maps) {
     const CUtensorMap* maps = m->upd_maps + size_t(m->parity) * m->G.nb * update_tma_maps_per_block();
     launch_update_tma(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, maps, m->upd_xoff, push);
+  } else if (m->G.dim == 3 && m->ph.prof == 0 &&
+             (m->upd_kind == 3 || (m->upd_kind == 2 && update_emf_fills(m->G, kr0, kr1)))) {
+    // two kernels: corner EMFs, then the cell update (not under phase
+    // profiling, which splits the fused kernel's time by its phases)
+    launch_update_emf(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, push);
   } else if (m->G.dim == 3 && m->upd_kind == 1) {
     launch_update_ws(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, push);
   } else {
@@ -790,7 +798,8 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   if (const char* e = std::getenv("PMHD_FLUX_SMEM_PAD")) m->fopt.pad = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("PMHD_FLUX_XY")) m->flux_xy = (std::atoi(e) == 1) ? 3 : (std::atoi(e) & 3);
   if (const char* e = std::getenv("PMHD_FLUX_CONC")) m->flux_conc = std::max(0, std::min(3, std::atoi(e)));
-  if (const char* e = std::getenv("PMHD_UPDATE")) m->upd_kind = (std::string(e) == "ws") ? 1 : 0;
+  if (const char* e = std::getenv("PMHD_UPDATE"))
+    m->upd_kind = (std::string(e) == "ws") ? 1 : (std::string(e) == "emf") ? 3 : 0;
   m->slab_ev.resize((G.ke - G.ks) / 8 + 2);
   for (auto& e : m->slab_ev) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   MCK(cudaStreamSynchronize(ctx->stream));

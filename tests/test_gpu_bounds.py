@@ -45,12 +45,15 @@ for name in names:
 
 # the default kernel selection, then the round-2 alternatives forced on these
 # small meshes: column / row march flux kernels, the x1 + x2 kernel, and the
-# TMA-staged and warp-specialised update kernels
+# TMA-staged, warp-specialised and two-kernel update forms
 VARIANTS = {
     "default": {},
     "march": {"PMHD_FLUX_MARCH": "2", "PMHD_FLUX_MARCH_X1": "1", "PMHD_FLUX_MARCH_STAGES": "3"},
     "xy_tma": {"PMHD_FLUX_XY": "1", "PMHD_UPDATE": "tma"},
     "march_ws": {"PMHD_FLUX_MARCH": "2", "PMHD_FLUX_MARCH_STAGES": "3", "PMHD_UPDATE": "ws"},
+    # the two-kernel update (edge EMFs + cell update), the default on meshes
+    # that fill the GPU, forced here
+    "march_emf": {"PMHD_FLUX_MARCH": "2", "PMHD_FLUX_MARCH_STAGES": "3", "PMHD_UPDATE": "emf"},
 }
 
 

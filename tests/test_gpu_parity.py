@@ -129,6 +129,15 @@ def test_fma_build_within_tolerance(gpu_available, name):
     assert g.divb_max() <= max(1e-11, 10 * o.divb_max())
 
 
+@pytest.mark.parametrize("name", [c for c in CASES if CASES[c][0].get("nx3", 1) > 1])
+def test_fma_build_emf_update_within_tolerance(gpu_available, name, monkeypatch):
+    """The two-kernel update (edge EMFs + cell update; the default on meshes
+    that fill the GPU, forced here on the small 3D cases) in the FMA build
+    stays within the oracle tolerance, as the fused kernel does."""
+    monkeypatch.setenv("PMHD_UPDATE", "emf")
+    test_fma_build_within_tolerance(gpu_available, name)
+
+
 @pytest.mark.parametrize("parity", [True, False])
 def test_linear_wave_l1_and_order_on_gpu(gpu_available, parity):
     """Identical linear-wave L1 error and convergence order as the oracle
@@ -257,12 +266,13 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
         assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
 
 
-@pytest.mark.parametrize("alt", ["tma", "ws"])
+@pytest.mark.parametrize("alt", ["tma", "ws", "emf"])
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "wave3d_tiny_blocks", "wave3d_ng3_ragged",
                                   "wave3d_ng4_8blk", "turb3d", "blast3d_64_floor"])
 def test_update_kernels_bitwise(gpu_available, case, alt, monkeypatch):
-    """The TMA-staged (PMHD_UPDATE=tma) and warp-specialised (PMHD_UPDATE=ws)
-    update kernels and the default LDG update kernel compute the same
+    """The TMA-staged (PMHD_UPDATE=tma), warp-specialised (PMHD_UPDATE=ws) and
+    two-kernel (PMHD_UPDATE=emf: corner EMFs, then the cell update) forms and
+    the default LDG update kernel compute the same
     expressions on the same operands: the
     parity build gives the same bits with either (the FMA build may contract
     a multiply-add differently in the two kernels; it is held to the oracle

@@ -8,5 +8,5 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 100 --csv --log-file gpurun_out/launches_256.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k "regex:k_update_fused|k_flux_fused|k_flux_march|k_flux_x1march" -s 0 -c 8 -o gpurun_out/prof_256 $CMD > gpurun_out/ncu.log 2>&1
+ncu --set full --clock-control none --import-source on -k "regex:k_update_fused|k_edge_emf|k_cell_update|k_flux_fused|k_flux_march|k_flux_x1march" -s 0 -c 10 -o gpurun_out/prof_256 $CMD > gpurun_out/ncu.log 2>&1
 cat gpurun_out/bench_ref.json gpurun_out/bench.json; tail -n 2 gpurun_out/bench.err gpurun_out/ncu.log
