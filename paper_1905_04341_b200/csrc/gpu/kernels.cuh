@@ -173,7 +173,8 @@ void update_ec_box(int box[2]);
 // where update_emf_fills (PMHD_UPDATE=emf: always, =ldg: never).
 bool update_emf_fills(const KGeom& G, int kr0, int kr1);
 void launch_update_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
-                       const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push);
+                       const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push,
+                       int all_local);
 void launch_update_ws(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks, const KStage* kd,
                       DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push);
 int update_tma_maps_per_block();

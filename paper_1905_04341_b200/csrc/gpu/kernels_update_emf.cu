@@ -42,18 +42,26 @@ __device__ __forceinline__ void STC(double* p, double v) { __stcs(p, v); }
 // [kr0, kr1], E3 at (i-1/2, j-1/2, k) for cell planes k in [kr0, kr1), each
 // stored at idx(kk, j, i) of w[0], w[1], w[2].  Plane kk-1's x2 ey / weight,
 // x1 ez / weight and cell-centred E are carried from the previous step.
+//
+// rim (every neighbour on this rank): the block's upper rim edges (i = ie,
+// j = je and, bit 1, kk = ke) are not formed here but stored by the upper
+// neighbour's threads on its lower rim (i = is, j = js, kk = ks), which form
+// the same edge from bit-identical operands (halo faces and cell E are exact
+// images of the neighbour's own), so the grid covers the owned range only.
 template <int SEG>
 __global__ void __launch_bounds__(CTHR, PMHD_EMF_MINB)
 k_edge_emf(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, const KStage* __restrict__ kd, int kr0,
-           int kr1) {
+           int kr1, int rim) {
   if (kd != nullptr && kd->skip) return;
-  const int nseg = (kr1 + 1 - kr0 + SEG - 1) / SEG;
+  const int kext = (rim & 2) ? kr1 : kr1 + 1;  // edge planes [kr0, kext)
+  const int nseg = (kext - kr0 + SEG - 1) / SEG;
   const int b = blockIdx.z / nseg;
   const int kb = kr0 + (int)(blockIdx.z % nseg) * SEG;
-  const int kend = min(kb + SEG, kr1 + 1);
+  const int kend = min(kb + SEG, kext);
   const int i = G.is + blockIdx.x * CX + threadIdx.x % CX;
   const int j = G.js + blockIdx.y * CY + threadIdx.x / CX;
-  if (i > G.ie || j > G.je) return;
+  const int r1 = rim & 1;
+  if (i > G.ie - r1 || j > G.je - r1) return;
   const DevBlock& B = blks[b];
   const double* __restrict__ X1e = B.fx[0][5];
   const double* __restrict__ X1b = B.fx[0][6];
@@ -85,15 +93,43 @@ k_edge_emf(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, const KStage* _
     const double cn = X1b[id], cwn = X1w[id];
     const double e0n = Ec0[id], e0mn = Ec0[id - sx];
     const double e1n = Ec1[id], e1mn = Ec1[id - 1];
-    if (i < G.ie)
-      STC(W1 + id, corner_emf(mode, an, a, X3b[id], X3b[id - sx], awn, aw, X3w[id], X3w[id - sx], e0n, e0mn,
-                              e0, e0m));
-    if (j < G.je)
-      STC(W2 + id, corner_emf(mode, X3e[id], X3e[id - 1], cn, c, X3w[id], X3w[id - 1], cwn, cw, e1n, e1,
-                              e1mn, e1m));
-    if (kk < kr1)
-      STC(W3 + id, corner_emf(mode, X1e[id], X1e[id - sx], X2b[id], X2b[id - 1], cwn, X1w[id - sx], awn,
-                              X2w[id - 1], Ec2[id], Ec2[id - 1], Ec2[id - sx], Ec2[id - sx - 1]));
+    double v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    if (i < G.ie) {
+      v1 = corner_emf(mode, an, a, X3b[id], X3b[id - sx], awn, aw, X3w[id], X3w[id - sx], e0n, e0mn, e0, e0m);
+      STC(W1 + id, v1);
+    }
+    if (j < G.je) {
+      v2 = corner_emf(mode, X3e[id], X3e[id - 1], cn, c, X3w[id], X3w[id - 1], cwn, cw, e1n, e1, e1mn, e1m);
+      STC(W2 + id, v2);
+    }
+    if (kk < kr1) {
+      v3 = corner_emf(mode, X1e[id], X1e[id - sx], X2b[id], X2b[id - 1], cwn, X1w[id - sx], awn, X2w[id - 1],
+                      Ec2[id], Ec2[id - 1], Ec2[id - sx], Ec2[id - sx - 1]);
+      STC(W3 + id, v3);
+    }
+    // lower-rim edges are also the lower neighbours' upper-rim edges
+    if (r1 && (i == G.is || j == G.js)) {
+      const int oi = G.mb[0], oj = G.mb[1] * sx;
+      if (i == G.is) {
+        const DevBlock& L = blks[B.nbr[0][0]];
+        STC(L.w[1] + id + oi, v2);
+        if (kk < kr1) STC(L.w[2] + id + oi, v3);
+        if (j == G.js && kk < kr1) STC(blks[L.nbr[1][0]].w[2] + id + oi + oj, v3);
+      }
+      if (j == G.js) {
+        const DevBlock& D = blks[B.nbr[1][0]];
+        STC(D.w[0] + id + oj, v1);
+        if (kk < kr1) STC(D.w[2] + id + oj, v3);
+      }
+    }
+    if ((rim & 2) && kk == G.ks) {
+      const int ok = G.mb[2] * sy;
+      const DevBlock& K = blks[B.nbr[2][0]];
+      STC(K.w[0] + id + ok, v1);
+      STC(K.w[1] + id + ok, v2);
+      if (i == G.is) STC(blks[blks[B.nbr[0][0]].nbr[2][0]].w[1] + id + G.mb[0] + ok, v2);
+      if (j == G.js) STC(blks[blks[B.nbr[1][0]].nbr[2][0]].w[0] + id + G.mb[1] * sx + ok, v1);
+    }
     a = an; aw = awn; c = cn; cw = cwn;
     e0 = e0n; e0m = e0mn; e1 = e1n; e1m = e1mn;
   }
@@ -254,12 +290,16 @@ bool update_emf_fills(const KGeom& G, int kr0, int kr1) {
 }
 
 void launch_update_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
-                       const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push) {
+                       const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push,
+                       int all_local) {
   constexpr int SEG = PMHD_EMF_SEG;
   {
-    const int nseg = (kr1 + 1 - kr0 + SEG - 1) / SEG;
-    const dim3 grid((G.ie - G.is + 1 + CX - 1) / CX, (G.je - G.js + 1 + CY - 1) / CY, nseg * G.nb);
-    k_edge_emf<SEG><<<grid, CTHR, 0, s>>>(blks, G, ph, kd, kr0, kr1);
+    // rim images need every neighbour on this rank; along k also the whole block
+    const int rim = all_local ? (1 | ((kr0 == G.ks && kr1 == G.ke) ? 2 : 0)) : 0;
+    const int r1 = rim & 1, kext = (rim & 2) ? kr1 : kr1 + 1;
+    const int nseg = (kext - kr0 + SEG - 1) / SEG;
+    const dim3 grid((G.ie - G.is + 1 - r1 + CX - 1) / CX, (G.je - G.js + 1 - r1 + CY - 1) / CY, nseg * G.nb);
+    k_edge_emf<SEG><<<grid, CTHR, 0, s>>>(blks, G, ph, kd, kr0, kr1, rim);
   }
   {
     const int nseg = (kr1 - kr0 + SEG - 1) / SEG;

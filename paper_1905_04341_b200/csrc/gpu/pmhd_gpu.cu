@@ -109,6 +109,7 @@ struct pmhd_mesh {
   // GPU, else the fused LDG kernel (default); 0 fused (PMHD_UPDATE=ldg), 1
   // warp-specialised (=ws), 3 two kernels always (=emf); tma: upd_maps
   int upd_kind = 2;
+  bool emf_rim = true;            // edge EMFs: upper-rim edges stored by the neighbours (PMHD_EMF_RIM=0: formed locally)
   std::vector<cudaEvent_t> slab_ev;
   cudaEvent_t ev[8] = {};
   cudaEvent_t xev[25] = {};        // host<->device transfer pipeline (one per staged array + 1)
@@ -301,7 +302,8 @@ void launch_update_any(pmhd_mesh* m, const KStage& ks, const KStage* kd, int wan
              (m->upd_kind == 3 || (m->upd_kind == 2 && update_emf_fills(m->G, kr0, kr1)))) {
     // two kernels: corner EMFs, then the cell update (not under phase
     // profiling, which splits the fused kernel's time by its phases)
-    launch_update_emf(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, push);
+    launch_update_emf(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, push,
+                      (m->all_local && m->emf_rim) ? 1 : 0);
   } else if (m->G.dim == 3 && m->upd_kind == 1) {
     launch_update_ws(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, push);
   } else {
@@ -798,6 +800,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   if (const char* e = std::getenv("PMHD_FLUX_SMEM_PAD")) m->fopt.pad = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("PMHD_FLUX_XY")) m->flux_xy = (std::atoi(e) == 1) ? 3 : (std::atoi(e) & 3);
   if (const char* e = std::getenv("PMHD_FLUX_CONC")) m->flux_conc = std::max(0, std::min(3, std::atoi(e)));
+  if (const char* e = std::getenv("PMHD_EMF_RIM")) m->emf_rim = std::atoi(e) != 0;
   if (const char* e = std::getenv("PMHD_UPDATE"))
     m->upd_kind = (std::string(e) == "ws") ? 1 : (std::string(e) == "emf") ? 3 : 0;
   m->slab_ev.resize((G.ke - G.ks) / 8 + 2);

@@ -266,7 +266,7 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
         assert np.array_equal(o.get_block(gid).u, g.get_block(gid).u)
 
 
-@pytest.mark.parametrize("alt", ["tma", "ws", "emf"])
+@pytest.mark.parametrize("alt", ["tma", "ws", "emf", "emf_norim"])
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "wave3d_tiny_blocks", "wave3d_ng3_ragged",
                                   "wave3d_ng4_8blk", "turb3d", "blast3d_64_floor"])
 def test_update_kernels_bitwise(gpu_available, case, alt, monkeypatch):
@@ -281,7 +281,9 @@ def test_update_kernels_bitwise(gpu_available, case, alt, monkeypatch):
     cfg = RunConfig(**kw)
     out = []
     for kern in ("ldg", alt):
-        monkeypatch.setenv("PMHD_UPDATE", kern)
+        # emf_norim: the edge-EMF kernel forms its upper-rim edges itself
+        monkeypatch.setenv("PMHD_EMF_RIM", "0" if kern == "emf_norim" else "1")
+        monkeypatch.setenv("PMHD_UPDATE", kern.split("_")[0])
         g = GpuSolver(cfg, parity=True)
         g.load_pgen()
         dt = g.new_dt()
