@@ -18,7 +18,10 @@ namespace pmhd_gpu {
 
 namespace {
 
-constexpr int CX = 32, CY = 4, CTHR = CX * CY;  // thread columns per CTA (i, j)
+#ifndef PMHD_EMF_CY
+#define PMHD_EMF_CY 4
+#endif
+constexpr int CX = 32, CY = PMHD_EMF_CY, CTHR = CX * CY;  // thread columns per CTA (i, j)
 #ifndef PMHD_EMF_SEG
 #define PMHD_EMF_SEG 16  // edge / cell planes marched by one CTA
 #endif
