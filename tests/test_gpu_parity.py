@@ -479,10 +479,13 @@ def test_multirank_halo_path_bitwise(gpu_available, nranks, stream_ordered, case
     p2p: remote faces read straight from the other engines' memory by the
     exchange kernels (pmhd_gpu_peer_attach), no pack / unpack.  march "2":
     the column-march x2 / x3 kernels forced on these small meshes, so their
-    interior / boundary split (the halo overlap) is covered too."""
+    interior / boundary split (the halo overlap) is covered too, and the
+    two-kernel update (edge EMFs + cell update; in 3D, without the rim
+    stores, since the neighbours are remote)."""
     from paper_1905_04341_b200.parallel import plan_for, LoopbackWorld
     monkeypatch.setenv("PMHD_FLUX_MARCH", march)
     monkeypatch.setenv("PMHD_FLUX_MARCH_STAGES", "3")
+    monkeypatch.setenv("PMHD_UPDATE", "emf" if march == "2" else "ldg")
     cfg = RunConfig(**MULTIRANK[case])
     plan = plan_for(cfg, nranks)
     engines = [GpuSolver(cfg, parity=True, gids=plan.local_gids(r)) for r in range(nranks)]
