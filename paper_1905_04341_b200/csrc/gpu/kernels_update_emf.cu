@@ -1,6 +1,6 @@
 // kernels_update_emf.cu -- the end of a VL2 stage as two barrier-free
-// kernels (3D meshes that fill the GPU: the default; PMHD_UPDATE=emf forces
-// it, PMHD_UPDATE=ldg selects k_update_fused), the same operations and operand
+// kernels (the default on 3D meshes; PMHD_UPDATE=ldg selects
+// k_update_fused, which 2D meshes use), the same operations and operand
 // order as k_update_fused (kernels_update.cu), so the parity build is
 // bit-identical to it and to the oracle:
 //   k_edge_emf    corner EMFs E1, E2, E3 (ct_emf) into three
@@ -283,19 +283,19 @@ k_cell_update(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_ar
 
 }  // namespace
 
-bool update_emf_fills(const KGeom& G, int kr0, int kr1) {
-  // at least two waves of cell-update CTAs at 8 per SM, as the fused kernel's
-  // 16-plane segments need (smaller meshes keep k_update_fused, which
-  // shortens its segments to fill the GPU)
-  const long long ctas = (long long)((G.ie - G.is + CX - 1) / CX) * ((G.je - G.js + CY - 1) / CY) *
-                         ((kr1 - kr0 + PMHD_EMF_SEG - 1) / PMHD_EMF_SEG) * G.nb;
-  return ctas >= 2LL * 148 * PMHD_CELL_MINB;
+namespace {
+// segment length: PMHD_EMF_SEG planes, or 4 / 1 when the mesh is too small
+// to give ~2 waves of cell-update CTAs at PMHD_CELL_MINB per SM otherwise
+int emf_seg(const KGeom& G, int kr0, int kr1) {
+  const int cols = ((G.ie - G.is + CX - 1) / CX) * ((G.je - G.js + CY - 1) / CY) * G.nb;
+  const int want = (2 * 148 * PMHD_CELL_MINB + cols - 1) / cols;  // segments per column
+  const int fit = (kr1 - kr0 + want - 1) / want;                    // planes per segment
+  return (fit >= PMHD_EMF_SEG) ? PMHD_EMF_SEG : (fit >= 4 ? 4 : 1);
 }
 
-void launch_update_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
-                       const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push,
-                       int all_local) {
-  constexpr int SEG = PMHD_EMF_SEG;
+template <int SEG>
+void launch_emf_seg(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks, const KStage* kd,
+                    DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push, int all_local) {
   {
     // rim images need every neighbour on this rank; along k also the whole block
     const int rim = all_local ? (1 | ((kr0 == G.ks && kr1 == G.ke) ? 2 : 0)) : 0;
@@ -309,6 +309,32 @@ void launch_update_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, co
     const dim3 grid((G.ie - G.is + CX - 1) / CX, (G.je - G.js + CY - 1) / CY, nseg * G.nb);
     k_cell_update<SEG><<<grid, CTHR, 0, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, push);
   }
+}
+}  // namespace
+
+bool update_emf_fills(const KGeom& G, int kr0, int kr1) {
+  // PMHD_EMF_SMALL=1 (default): every 3D mesh, the segments shortened to
+  // fill the GPU; 0: only meshes that fill it with full-length segments
+  // (smaller ones keep k_update_fused)
+#ifndef PMHD_EMF_SMALL
+#define PMHD_EMF_SMALL 1
+#endif
+  if (PMHD_EMF_SMALL) return true;
+  const long long ctas = (long long)((G.ie - G.is + CX - 1) / CX) * ((G.je - G.js + CY - 1) / CY) *
+                         ((kr1 - kr0 + PMHD_EMF_SEG - 1) / PMHD_EMF_SEG) * G.nb;
+  return ctas >= 2LL * 148 * PMHD_CELL_MINB;
+}
+
+void launch_update_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
+                       const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push,
+                       int all_local) {
+  const int seg = emf_seg(G, kr0, kr1);
+  if (seg == PMHD_EMF_SEG)
+    launch_emf_seg<PMHD_EMF_SEG>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, s, push, all_local);
+  else if (seg == 4)
+    launch_emf_seg<4>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, s, push, all_local);
+  else
+    launch_emf_seg<1>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, s, push, all_local);
 }
 
 }  // namespace pmhd_gpu

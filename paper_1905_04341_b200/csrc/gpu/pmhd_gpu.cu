@@ -105,8 +105,8 @@ struct pmhd_mesh {
   // (+0.6-0.8 % at 256^3). PMHD_FLUX_CONC: 0 off, 1 x2 (default), 2 x3, 3 x2 and x3
   int flux_conc = 1;
   cudaEvent_t ev_fx[3] = {};
-  // 3D update: 2 two kernels (edge EMFs + cell update) where they fill the
-  // GPU, else the fused LDG kernel (default); 0 fused (PMHD_UPDATE=ldg), 1
+  // 3D update: 2 two kernels (edge EMFs + cell update; default, see
+  // update_emf_fills), 0 fused (PMHD_UPDATE=ldg; 2D always), 1
   // warp-specialised (=ws), 3 two kernels always (=emf); tma: upd_maps
   int upd_kind = 2;
   bool emf_rim = true;            // edge EMFs: upper-rim edges stored by the neighbours (PMHD_EMF_RIM=0: formed locally)
