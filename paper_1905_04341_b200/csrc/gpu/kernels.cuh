@@ -169,8 +169,8 @@ void update_ec_box(int box[2]);
 // alignment of the map base).
 // warp-specialised update kernel (kernels_update_ws.cu, 3D)
 // Two barrier-free kernels (corner EMFs, then CT + conserved update + c2p + dt;
-// 3D): the corner EMFs go through the block's w[0..2] arrays.  The default
-// where update_emf_fills (every 3D mesh unless built with
+// in 2D only E3 is formed): the corner EMFs go through the block's w[0..2]
+// arrays.  The default where update_emf_fills (every mesh unless built with
 // PMHD_EMF_SMALL=0; PMHD_UPDATE=emf: always, =ldg: never).
 bool update_emf_fills(const KGeom& G, int kr0, int kr1);
 void launch_update_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,

@@ -1,6 +1,6 @@
 // kernels_update_emf.cu -- the end of a VL2 stage as two barrier-free
-// kernels (the default on 3D meshes; PMHD_UPDATE=ldg selects
-// k_update_fused, which 2D meshes use), the same operations and operand
+// kernels (the default; PMHD_UPDATE=ldg selects k_update_fused), the same
+// operations and operand
 // order as k_update_fused (kernels_update.cu), so the parity build is
 // bit-identical to it and to the oracle:
 //   k_edge_emf    corner EMFs E1, E2, E3 (ct_emf) into three
@@ -138,12 +138,45 @@ k_edge_emf(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, const KStage* _
   }
 }
 
+// 2D: E3 of the one cell plane; E1 / E2 are the x2 / x1 face values
+// themselves (the cell kernel reads them from the face arrays).  Rim stores
+// as k_edge_emf.
+__global__ void __launch_bounds__(CTHR, PMHD_EMF_MINB)
+k_edge_emf2d(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, const KStage* __restrict__ kd, int rim) {
+  if (kd != nullptr && kd->skip) return;
+  const int b = blockIdx.z;
+  const int i = G.is + blockIdx.x * CX + threadIdx.x % CX;
+  const int j = G.js + blockIdx.y * CY + threadIdx.x / CX;
+  const int r1 = rim & 1;
+  if (i > G.ie - r1 || j > G.je - r1) return;
+  const DevBlock& B = blks[b];
+  const int sx = G.sx, id = G.idx(G.ks, j, i);
+  PMHD_CHECK_ID(G, id - sx - 1);
+  const double* __restrict__ X1e = B.fx[0][5];
+  const double* __restrict__ X1w = B.fx[0][7];
+  const double* __restrict__ X2b = B.fx[1][6];
+  const double* __restrict__ X2w = B.fx[1][7];
+  const double* __restrict__ Ec2 = B.ec[2];
+  const double v3 = corner_emf(ph.emf, X1e[id], X1e[id - sx], X2b[id], X2b[id - 1], X1w[id], X1w[id - sx],
+                               X2w[id], X2w[id - 1], Ec2[id], Ec2[id - 1], Ec2[id - sx], Ec2[id - sx - 1]);
+  STC(B.w[2] + id, v3);
+  if (r1 && (i == G.is || j == G.js)) {
+    const int oi = G.mb[0], oj = G.mb[1] * sx;
+    if (i == G.is) {
+      const DevBlock& L = blks[B.nbr[0][0]];
+      STC(L.w[2] + id + oi, v3);
+      if (j == G.js) STC(blks[L.nbr[1][0]].w[2] + id + oi + oj, v3);
+    }
+    if (j == G.js) STC(blks[B.nbr[1][0]].w[2] + id + oj, v3);
+  }
+}
+
 // CT faces, conserved update, cons_to_prim and dt of thread column (i, j),
 // i in [is, ie), j in [js, je), cell planes [kr0, kr1).  The column's lower
 // faces (and, on the block's upper rim, its upper faces) are stored; the
 // upper faces are also formed here for the cell-centred field.  b3 at face
 // k+1 is carried to the next plane.
-template <int SEG>
+template <int SEG, bool D3>
 __global__ void __launch_bounds__(CTHR, PMHD_CELL_MINB)
 k_cell_update(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_arg,
               const KStage* __restrict__ kd, DevRed* red, int want_dt, int kr0, int kr1, int push) {
@@ -166,8 +199,9 @@ k_cell_update(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_ar
     double* const* X1 = B.fx[0];
     double* const* X2 = B.fx[1];
     double* const* X3 = B.fx[2];
-    const double* __restrict__ E1 = B.w[0];
-    const double* __restrict__ E2 = B.w[1];
+    // E1 / E2: the edge arrays (3D) or, in 2D, the x2 / x1 face values
+    const double* __restrict__ E1 = D3 ? B.w[0] : B.fx[1][5];
+    const double* __restrict__ E2 = D3 ? B.w[1] : B.fx[0][6];
     const double* __restrict__ E3 = B.w[2];
     double* const* PL = push ? blks[B.nbr[0][0]].st[ks.out_sel] : nullptr;
     double* const* PR = push ? blks[B.nbr[0][1]].st[ks.out_sel] : nullptr;
@@ -186,7 +220,7 @@ k_cell_update(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_ar
 #if PMHD_CELL_CARRY_X3
     double f3[5];
 #pragma unroll
-    for (int v = 0; v < 5; ++v) f3[v] = X3[v][id];
+    for (int v = 0; v < 5; ++v) f3[v] = D3 ? X3[v][id] : 0.0;
 #endif
     for (int k = kb; k < kend; ++k, id += sy) {
       PMHD_CHECK_ID(G, id + sy + sx + 1);
@@ -194,12 +228,22 @@ k_cell_update(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_ar
       const double n2 = E2[id + sy], n2p = E2[id + 1 + sy], n1 = E1[id + sy], n1p = E1[id + sx + sy];
 #else
       const double q2 = E2[id], q2p = E2[id + 1], q1 = E1[id], q1p = E1[id + sx];
-      const double n2 = E2[id + sy], n2p = E2[id + 1 + sy], n1 = E1[id + sy], n1p = E1[id + sx + sy];
+      // edge plane k+1 (2D: both b3 layers use the plane-k edges)
+      const double n2 = D3 ? E2[id + sy] : q2, n2p = D3 ? E2[id + 1 + sy] : q2p;
+      const double n1 = D3 ? E1[id + sy] : q1, n1p = D3 ? E1[id + sx + sy] : q1p;
 #endif
-      const double b1lo = Sb[5][id] - (c2 * (E3[id + sx] - E3[id]) - c3 * (n2 - q2));
-      const double b1hi = Sb[5][id + 1] - (c2 * (E3[id + 1 + sx] - E3[id + 1]) - c3 * (n2p - q2p));
-      const double b2lo = Sb[6][id] - (c3 * (n1 - q1) - c1 * (E3[id + 1] - E3[id]));
-      const double b2hi = Sb[6][id + sx] - (c3 * (n1p - q1p) - c1 * (E3[id + sx + 1] - E3[id + sx]));
+      double b1lo, b1hi, b2lo, b2hi;
+      if (D3) {
+        b1lo = Sb[5][id] - (c2 * (E3[id + sx] - E3[id]) - c3 * (n2 - q2));
+        b1hi = Sb[5][id + 1] - (c2 * (E3[id + 1 + sx] - E3[id + 1]) - c3 * (n2p - q2p));
+        b2lo = Sb[6][id] - (c3 * (n1 - q1) - c1 * (E3[id + 1] - E3[id]));
+        b2hi = Sb[6][id + sx] - (c3 * (n1p - q1p) - c1 * (E3[id + sx + 1] - E3[id + sx]));
+      } else {
+        b1lo = Sb[5][id] - c2 * (E3[id + sx] - E3[id]);
+        b1hi = Sb[5][id + 1] - c2 * (E3[id + 1 + sx] - E3[id + 1]);
+        b2lo = Sb[6][id] + c1 * (E3[id + 1] - E3[id]);
+        b2hi = Sb[6][id + sx] + c1 * (E3[id + sx + 1] - E3[id + sx]);
+      }
       const double b3hi = Sb[7][id + sy] - (c1 * (n2p - n2) - c2 * (n1p - n1));
 #if PMHD_CELL_CARRY_E
       q2 = n2; q2p = n2p; q1 = n1; q1p = n1p;
@@ -228,13 +272,15 @@ k_cell_update(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_ar
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         double du = c1 * (X1[v][id + 1] - X1[v][id]) + c2 * (X2[v][id + sx] - X2[v][id]);
+        if (D3) {
 #if PMHD_CELL_CARRY_X3
-        const double f3n = X3[v][id + sy];
-        du = du + c3 * (f3n - f3[v]);
-        f3[v] = f3n;
+          const double f3n = X3[v][id + sy];
+          du = du + c3 * (f3n - f3[v]);
+          f3[v] = f3n;
 #else
-        du = du + c3 * (X3[v][id + sy] - X3[v][id]);
+          du = du + c3 * (X3[v][id + sy] - X3[v][id]);
 #endif
+        }
         u[v] = Sb[v][id] - du;
       }
       double bc[3], w[8];
@@ -248,7 +294,7 @@ k_cell_update(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_ar
       if (fl & 4) {
         const long long gi = (long long)B.c[0] * G.mb[0] + (i - G.is);
         const long long gj = (long long)B.c[1] * G.mb[1] + (j - G.js);
-        const long long gk = (long long)B.c[2] * G.mb[2] + (k - G.ks);
+        const long long gk = D3 ? (long long)B.c[2] * G.mb[2] + (k - G.ks) : 0;
         atomicMin(&red[ks.stage].bad_key, (unsigned long long)((gk * G.nx[1] + gj) * G.nx[0] + gi));
       }
 #pragma unroll
@@ -262,8 +308,10 @@ k_cell_update(const DevBlock* __restrict__ blks, KGeom G, KPhys ph, KStage ks_ar
         const double cf1 = fast_speed_n(d, p, w[5], w[6], w[7], ph.gamma);
         const double cf2 = fast_speed_n(d, p, w[6], w[7], w[5], ph.gamma);
         double t = fmin(ddiv(G.dx[0], fabs(w[1]) + cf1), ddiv(G.dx[1], fabs(w[2]) + cf2));
-        const double cf3 = fast_speed_n(d, p, w[7], w[5], w[6], ph.gamma);
-        t = fmin(t, ddiv(G.dx[2], fabs(w[3]) + cf3));
+        if (D3) {
+          const double cf3 = fast_speed_n(d, p, w[7], w[5], w[6], ph.gamma);
+          t = fmin(t, ddiv(G.dx[2], fabs(w[3]) + cf3));
+        }
         tmin = fmin(tmin, t);
       }
       b3lo = b3hi;
@@ -307,7 +355,7 @@ void launch_emf_seg(const DevBlock* blks, const KGeom& G, const KPhys& ph, const
   {
     const int nseg = (kr1 - kr0 + SEG - 1) / SEG;
     const dim3 grid((G.ie - G.is + CX - 1) / CX, (G.je - G.js + CY - 1) / CY, nseg * G.nb);
-    k_cell_update<SEG><<<grid, CTHR, 0, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, push);
+    k_cell_update<SEG, true><<<grid, CTHR, 0, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, push);
   }
 }
 }  // namespace
@@ -328,6 +376,14 @@ bool update_emf_fills(const KGeom& G, int kr0, int kr1) {
 void launch_update_emf(const DevBlock* blks, const KGeom& G, const KPhys& ph, const KStage& ks,
                        const KStage* kd, DevRed* red, int want_dt, int kr0, int kr1, cudaStream_t s, int push,
                        int all_local) {
+  if (G.dim == 2) {  // one cell plane: E3, then the cell update
+    const int r1 = all_local ? 1 : 0;
+    const dim3 ge((G.ie - G.is + 1 - r1 + CX - 1) / CX, (G.je - G.js + 1 - r1 + CY - 1) / CY, G.nb);
+    k_edge_emf2d<<<ge, CTHR, 0, s>>>(blks, G, ph, kd, r1);
+    const dim3 gc((G.ie - G.is + CX - 1) / CX, (G.je - G.js + CY - 1) / CY, G.nb);
+    k_cell_update<1, false><<<gc, CTHR, 0, s>>>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, push);
+    return;
+  }
   const int seg = emf_seg(G, kr0, kr1);
   if (seg == PMHD_EMF_SEG)
     launch_emf_seg<PMHD_EMF_SEG>(blks, G, ph, ks, kd, red, want_dt, kr0, kr1, s, push, all_local);

@@ -105,8 +105,8 @@ struct pmhd_mesh {
   // (+0.6-0.8 % at 256^3). PMHD_FLUX_CONC: 0 off, 1 x2 (default), 2 x3, 3 x2 and x3
   int flux_conc = 1;
   cudaEvent_t ev_fx[3] = {};
-  // 3D update: 2 two kernels (edge EMFs + cell update; default, see
-  // update_emf_fills), 0 fused (PMHD_UPDATE=ldg; 2D always), 1
+  // stage update: 2 two kernels (edge EMFs + cell update; default, see
+  // update_emf_fills), 0 fused (PMHD_UPDATE=ldg), 1
   // warp-specialised (=ws), 3 two kernels always (=emf); tma: upd_maps
   int upd_kind = 2;
   bool emf_rim = true;            // edge EMFs: upper-rim edges stored by the neighbours (PMHD_EMF_RIM=0: formed locally)
@@ -290,16 +290,21 @@ int build_update_maps(pmhd_mesh* m) {
   return PMHD_OK;
 }
 
-// The fused update kernel of one stage over planes [kr0, kr1): the
-// TMA-staged kernel when its maps exist (3D, PMHD_UPDATE=tma), else the LDG
-// kernel (default).
+// Whether the stage update runs as the two kernels (edge EMFs + cell update)
+bool update_two_kernels(const pmhd_mesh* m, int kr0, int kr1) {
+  return !m->upd_maps && m->G.dim >= 2 && m->ph.prof == 0 &&
+         (m->upd_kind == 3 || (m->upd_kind == 2 && update_emf_fills(m->G, kr0, kr1)));
+}
+
+// The update of one stage over planes [kr0, kr1): the TMA-staged kernel when
+// its maps exist (3D, PMHD_UPDATE=tma), the two kernels (default), the
+// warp-specialised kernel (PMHD_UPDATE=ws) or the fused LDG kernel.
 void launch_update_any(pmhd_mesh* m, const KStage& ks, const KStage* kd, int want_dt, int kr0, int kr1,
                        cudaStream_t st, int push) {
   if (m->upd_maps) {
     const CUtensorMap* maps = m->upd_maps + size_t(m->parity) * m->G.nb * update_tma_maps_per_block();
     launch_update_tma(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, maps, m->upd_xoff, push);
-  } else if (m->G.dim == 3 && m->ph.prof == 0 &&
-             (m->upd_kind == 3 || (m->upd_kind == 2 && update_emf_fills(m->G, kr0, kr1)))) {
+  } else if (update_two_kernels(m, kr0, kr1)) {
     // two kernels: corner EMFs, then the cell update (not under phase
     // profiling, which splits the fused kernel's time by its phases)
     launch_update_emf(m->dblk, m->G, m->ph, ks, kd, m->dred, want_dt, kr0, kr1, st, push,
@@ -404,7 +409,8 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     CK(cudaEventRecord(m->slab_ev[nslab], ctx->stream2));
     CK(cudaStreamWaitEvent(st, m->slab_ev[nslab], 0));
     if (do_exchange) launch_exchange(m->dblk, G, ks.out_sel, st, kd);
-    m->times.kernel_launches += nslab * (1 + G.dim) + (do_exchange ? G.dim : 0);
+    m->times.kernel_launches += nslab * ((update_two_kernels(m, G.ks, G.ks + S) ? 2 : 1) + G.dim) +
+                                (do_exchange ? G.dim : 0);
   } else {
     rec(m, 0);
     if (m->variant == 1) launch_c2p_all(m->dblk, G, m->ph, ks.in_sel, m->dred, s, st);
@@ -460,7 +466,8 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     if (do_exchange)
       for (int dir = d0; dir < G.dim; ++dir) launch_exchange_dir(m->dblk, G, ks.out_sel, dir, st, kd);
     rec(m, 5);
-    m->times.kernel_launches += ((m->variant == 0) ? 1 + G.dim - (xy ? 1 : 0) : 4 + G.dim) + (do_exchange ? G.dim - d0 : 0);
+    const int nupd = update_two_kernels(m, G.ks, G.ke) ? 2 : 1;
+    m->times.kernel_launches += ((m->variant == 0) ? nupd + G.dim - (xy ? 1 : 0) : 4 + G.dim) + (do_exchange ? G.dim - d0 : 0);
   }
   CK(cudaGetLastError());
   if (s == 2) {  // u^{n+1} (st[2]) becomes the current state: flip the tables
@@ -1065,7 +1072,8 @@ int graph_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, int
   // cycles that ran: the completed ones, plus the failing one (its stages ran
   // and flipped the tables inside the graph)
   const int ran = c.cycles + (c.err_key != ULLONG_MAX ? 1 : 0);
-  const long long per_cycle = 2 * (2 * G.dim + 1 - (m->push_x1 ? 1 : 0)) + 2 - (use_flux_xy(m, 1) ? 1 : 0) -
+  const long long per_cycle = 2 * (2 * G.dim + (update_two_kernels(m, G.ks, G.ke) ? 2 : 1) -
+                                   (m->push_x1 ? 1 : 0)) + 2 - (use_flux_xy(m, 1) ? 1 : 0) -
                               (use_flux_xy(m, 2) ? 1 : 0);
   m->times.kernel_launches += per_cycle * ran;
   if (ran & 1) {  // the state is in the other table after an odd number of cycles

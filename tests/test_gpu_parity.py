@@ -129,12 +129,12 @@ def test_fma_build_within_tolerance(gpu_available, name):
     assert g.divb_max() <= max(1e-11, 10 * o.divb_max())
 
 
-@pytest.mark.parametrize("name", [c for c in CASES if CASES[c][0].get("nx3", 1) > 1])
-def test_fma_build_emf_update_within_tolerance(gpu_available, name, monkeypatch):
-    """The two-kernel update (edge EMFs + cell update; the default on meshes
-    that fill the GPU, forced here on the small 3D cases) in the FMA build
-    stays within the oracle tolerance, as the fused kernel does."""
-    monkeypatch.setenv("PMHD_UPDATE", "emf")
+@pytest.mark.parametrize("name", list(CASES))
+def test_fma_build_fused_update_within_tolerance(gpu_available, name, monkeypatch):
+    """The fused update kernel (PMHD_UPDATE=ldg; the two-kernel update is the
+    default in 2D and 3D) in the FMA build stays within the oracle tolerance,
+    as the default does."""
+    monkeypatch.setenv("PMHD_UPDATE", "ldg")
     test_fma_build_within_tolerance(gpu_available, name)
 
 
@@ -268,7 +268,7 @@ def test_kernel_variants_bitwise(gpu_available, variant, monkeypatch):
 
 @pytest.mark.parametrize("alt", ["tma", "ws", "emf", "emf_norim"])
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "wave3d_tiny_blocks", "wave3d_ng3_ragged",
-                                  "wave3d_ng4_8blk", "turb3d", "blast3d_64_floor"])
+                                  "wave3d_ng4_8blk", "turb3d", "blast3d_64_floor", "ot2d_ragged", "ot2d_4blk"])
 def test_update_kernels_bitwise(gpu_available, case, alt, monkeypatch):
     """The TMA-staged (PMHD_UPDATE=tma), warp-specialised (PMHD_UPDATE=ws) and
     two-kernel (PMHD_UPDATE=emf: corner EMFs, then the cell update) forms and
