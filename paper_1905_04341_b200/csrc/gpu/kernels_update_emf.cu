@@ -1,8 +1,7 @@
 // kernels_update_emf.cu -- the end of a VL2 stage as two barrier-free
-// kernels (the default; PMHD_UPDATE=ldg selects k_update_fused), the same
-// operations and operand
-// order as k_update_fused (kernels_update.cu), so the parity build is
-// bit-identical to it and to the oracle:
+// kernels (the default; PMHD_UPDATE=ldg selects k_update_fused), with the
+// same operations and operand order as k_update_fused (kernels_update.cu),
+// so the parity build is bit-identical to it and to the oracle:
 //   k_edge_emf    corner EMFs E1, E2, E3 (ct_emf) into three
 //                 scratch arrays (the block's primitive arrays w[0..2], which
 //                 only the split debug variant uses);
@@ -11,7 +10,9 @@
 //                 face_to_center_b + cons_to_prim with floors / errors and
 //                 the dt partial min, one thread per (i, j) column.
 // Both march k with one thread per column and carry what plane k shares with
-// plane k+1 in registers; no shared memory, no barriers.
+// plane k+1 in registers; no shared memory, no barriers.  In 2D
+// k_edge_emf2d forms E3 only (E1 / E2 are the face values themselves).
+// Measurements: DESIGN.md section 4a ("Two-kernel stage update").
 #include "kernels.cuh"
 
 namespace pmhd_gpu {
