@@ -105,6 +105,13 @@ struct pmhd_mesh {
   // (+0.6-0.8 % at 256^3). PMHD_FLUX_CONC: 0 off, 1 x2 (default), 2 x3, 3 x2 and x3
   int flux_conc = 1;
   cudaEvent_t ev_fx[3] = {};
+  // stage-1 x2 / x3 ghost exchanges on stream3, overlapping the stage-2 x1
+  // flux launch (which reads no x2 / x3 ghosts with owned-face reuse); the
+  // x2 / x3 flux launches wait for ev_ex[d].  PMHD_EARLY_X1: 0 off, 1 on
+  // meshes up to 2^24 cells per rank (default), 2 always.
+  int early_x1 = 1;
+  bool ex_pending = false;
+  cudaEvent_t ev_ex[3] = {};
   // stage update: 2 two kernels (edge EMFs + cell update; default, see
   // update_emf_fills), 0 fused (PMHD_UPDATE=ldg), 1
   // warp-specialised (=ws), 3 two kernels always (=emf); tma: upd_maps
@@ -368,7 +375,7 @@ int prefetch_stage(pmhd_mesh* m, int s, double dt) {
 // device_ks: the kernels read the coefficients (and the skip flag) from the
 // device copy k_cycle_begin writes in a captured cycle; else by value.
 int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool prefetch_next = false,
-                  bool device_ks = false) {
+                  bool device_ks = false, bool early_ok = false) {
   pmhd_ctx* ctx = m->ctx;
   const KGeom& G = m->G;
   const KStage ks = make_stage(G, s, dt);
@@ -433,11 +440,18 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
       if (cdir == 3) CK(cudaStreamWaitEvent(ctx->stream3, m->ev_fx[0], 0));
     }
     for (int dir = xy ? 2 : 0; dir < G.dim; ++dir) {
+      // a pending stage-1 exchange of direction dir must be done first (x1:
+      // pushed by the update kernel, no wait)
+      if (m->ex_pending && dir >= 1) CK(cudaStreamWaitEvent(fst[dir], m->ev_ex[dir], 0));
       if (m->variant == 0)
         launch_flux_fused(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], kd, s, m->dred, 0, 1,
                           nk, fst[dir], flux_region, m->fopt);
       else
         launch_flux(m->dblk, G, m->ph, dir, ks.in_sel, ks.plm, ks.c1024[dir], st);
+    }
+    if (m->ex_pending) {  // (joined through the x2 / x3 launches; stream3 fully)
+      CK(cudaStreamWaitEvent(st, m->ev_ex[G.dim - 1], 0));
+      m->ex_pending = false;
     }
     if (cdir > 0) {
       CK(cudaEventRecord(m->ev_fx[1], ctx->stream2));
@@ -463,8 +477,27 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     }
     // (x1 ghosts already stored by the update kernel when pushed)
     const int d0 = (m->variant == 0 && m->push_x1) ? 1 : 0;
-    if (do_exchange)
+    // stage 1 of a step: the x2 / x3 exchanges on stream3, so the stage-2 x1
+    // flux launch (owned faces only: no x2 / x3 ghosts read) overlaps them
+    // (not with the fused x1 + x2 launch of stage 2, which needs the x2
+    // ghosts; measured +2 % on the 64^3 wave, +1 % on 512^2 Orszag-Tang, 0 to
+    // +0.2 % at 256^3 and -0.2 % on the 512^3 turbulence in 64 blocks, so
+    // meshes up to 2^24 cells per rank; PMHD_EARLY_X1=0 / 2: never / always)
+    const long long cells = (long long)G.mb[0] * G.mb[1] * G.mb[2] * G.nb;
+    const bool early = early_ok && s == 1 && do_exchange && d0 == 1 && m->face_reuse && m->variant == 0 &&
+                       !m->prof && !(prefetch_next && can_prefetch(m)) && !use_flux_xy(m, 2) &&
+                       (m->early_x1 == 2 || (m->early_x1 == 1 && cells <= (1LL << 24)));
+    if (early) {
+      CK(cudaEventRecord(m->ev_ex[0], st));
+      CK(cudaStreamWaitEvent(ctx->stream3, m->ev_ex[0], 0));
+      for (int dir = 1; dir < G.dim; ++dir) {
+        launch_exchange_dir(m->dblk, G, ks.out_sel, dir, ctx->stream3, kd);
+        CK(cudaEventRecord(m->ev_ex[dir], ctx->stream3));
+      }
+      m->ex_pending = true;
+    } else if (do_exchange) {
       for (int dir = d0; dir < G.dim; ++dir) launch_exchange_dir(m->dblk, G, ks.out_sel, dir, st, kd);
+    }
     rec(m, 5);
     const int nupd = update_two_kernels(m, G.ks, G.ke) ? 2 : 1;
     m->times.kernel_launches += ((m->variant == 0) ? nupd + G.dim - (xy ? 1 : 0) : 4 + G.dim) + (do_exchange ? G.dim - d0 : 0);
@@ -510,6 +543,11 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
 }
 
 int finish(pmhd_mesh* m, int stage_lo, int stage_hi, double* dt_next, pmhd_status* st) {
+  if (m->ex_pending) {  // (only if a stage 2 did not follow its stage 1)
+    pmhd_ctx* ctx = m->ctx;
+    CK(cudaStreamWaitEvent(ctx->stream, m->ev_ex[m->G.dim - 1], 0));
+    m->ex_pending = false;
+  }
   int rc = fetch_red(m);
   if (rc) return rc;
   pmhd_status s{};
@@ -778,6 +816,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   for (auto& e : m->ev) MCK(cudaEventCreate(&e));
   for (auto& e : m->ev_pre) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : m->ev_fx) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : m->ev_ex) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : m->xev) MCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // Overlap pays where the exchange is a real transfer (remote neighbours,
   // NCCL); with all neighbours local the exchange kernels take ~3 % of a
@@ -806,6 +845,7 @@ int pmhd_gpu_mesh_create(pmhd_ctx* ctx, const pmhd_mesh_desc* desc, const int* g
   if (const char* e = std::getenv("PMHD_FLUX_MARCH_STAGES")) m->fopt.march_stages = std::atoi(e) & 3;
   if (const char* e = std::getenv("PMHD_FLUX_SMEM_PAD")) m->fopt.pad = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("PMHD_FLUX_XY")) m->flux_xy = (std::atoi(e) == 1) ? 3 : (std::atoi(e) & 3);
+  if (const char* e = std::getenv("PMHD_EARLY_X1")) m->early_x1 = std::max(0, std::min(2, std::atoi(e)));
   if (const char* e = std::getenv("PMHD_FLUX_CONC")) m->flux_conc = std::max(0, std::min(3, std::atoi(e)));
   if (const char* e = std::getenv("PMHD_EMF_RIM")) m->emf_rim = std::atoi(e) != 0;
   if (const char* e = std::getenv("PMHD_UPDATE"))
@@ -837,6 +877,7 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   for (auto& e : m->slab_ev) if (e) cudaEventDestroy(e);
   for (auto& e : m->ev_pre) if (e) cudaEventDestroy(e);
   for (auto& e : m->ev_fx) if (e) cudaEventDestroy(e);
+  for (auto& e : m->ev_ex) if (e) cudaEventDestroy(e);
   for (auto& e : m->xev) if (e) cudaEventDestroy(e);
   delete m;
   return PMHD_OK;
@@ -985,7 +1026,7 @@ int pmhd_gpu_vl2_step(pmhd_mesh* m, double dt, double* dt_next, pmhd_status* st)
   if (int rc_ = use_device(m->ctx)) return rc_;
   if (!m->all_local) return fail(m->ctx, PMHD_ERR_INPUT, "step needs all neighbours local");
   int rc = reset_red(m);
-  if (!rc) rc = enqueue_stage(m, 1, dt, true, true);  // + stage-2 interior tiles over the exchange
+  if (!rc) rc = enqueue_stage(m, 1, dt, true, true, false, true);  // + stage-2 interior tiles over the exchange
   if (!rc) rc = enqueue_stage(m, 2, dt);
   if (rc) return rc;
   return finish(m, 1, 2, dt_next, st);
@@ -1017,7 +1058,7 @@ int capture_cycles(pmhd_mesh* m) {
   int rc = PMHD_OK;
   for (int c = 0; c < 2 && !rc; ++c) {  // two cycles: the tables flip once per cycle
     launch_cycle_begin(m->dctl, m->dks, m->dred, ctx->stream);
-    rc = enqueue_stage(m, 1, 0.0, true, false, true);
+    rc = enqueue_stage(m, 1, 0.0, true, false, true, true);
     if (!rc) rc = enqueue_stage(m, 2, 0.0, true, false, true);
     launch_cycle_end(m->dctl, m->dks, m->dred, ctx->stream);
   }

@@ -408,6 +408,31 @@ def test_flux_streams_bitwise(gpu_available, case, conc, monkeypatch):
                 assert np.array_equal(getattr(b0, f), getattr(b1, f)), (case, f)
 
 
+@pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_ragged", "turb3d", "wave3d_tiny_blocks"])
+def test_early_x1_flux_bitwise(gpu_available, case, monkeypatch):
+    """The stage-1 x2 / x3 ghost exchanges on a third stream, overlapping the
+    stage-2 x1 flux launch (PMHD_EARLY_X1, on for meshes up to 2^24 cells),
+    give the serial order's bits in the product build, also when the run
+    loop replays the cycle as a CUDA graph."""
+    kw, ncyc = CASES[case]
+    cfg = RunConfig(**kw)
+    out = []
+    for e in ("0", "1"):
+        monkeypatch.setenv("PMHD_EARLY_X1", e)
+        g = GpuSolver(cfg)
+        g.load_pgen()
+        dt = g.new_dt()
+        dts = []
+        for _ in range(ncyc):
+            dt, _st = g.vl2_step(dt)
+            dts.append(dt)
+        out.append((dts, [g.get_block(gid) for gid in range(cfg.nblocks)]))
+    assert out[0][0] == out[1][0]
+    for b0, b1 in zip(out[0][1], out[1][1]):
+        for f in ("u", "b1f", "b2f", "b3f"):
+            assert np.array_equal(getattr(b0, f), getattr(b1, f)), (case, f)
+
+
 @pytest.mark.parametrize("march", ["1", "2"])
 @pytest.mark.parametrize("case", ["wave3d_4blk", "blast3d_8blk_floor", "ot2d_4blk"])
 def test_overlap_prefetch_bitwise(gpu_available, case, march, monkeypatch):

@@ -12,6 +12,8 @@ for v in "$@"; do
     b128ldg) PMHD_UPDATE=ldg $B --block 128 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     emf) PMHD_UPDATE=emf $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     emf-*) PMHD_UPDATE=emf PMHD_GPU_LIB=paper_1905_04341_b200/lib/exp/libpmhd_gpu_${v#emf-}.so $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    ex0) PMHD_EARLY_X1=0 $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
+    m5ex0) PMHD_EARLY_X1=0 $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     conc*) PMHD_FLUX_CONC=${v#conc} $B > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     m5conc*) PMHD_FLUX_CONC=${v#m5conc} $B --workload m5 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
     b128conc*) PMHD_FLUX_CONC=${v#b128conc} $B --block 128 > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err ;;
