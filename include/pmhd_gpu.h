@@ -257,7 +257,8 @@ int pmhd_gpu_region_times(pmhd_mesh* mesh, pmhd_region_times* out, int reset);
 /* The context's CUDA stream (cudaStream_t) for interop: callers may record
  * events on it to time ABI calls.  Every call's device work is ordered on
  * it: work a call forks to the context's internal streams (the x2 flux
- * launch beside x1 -> x3, host<->device copies, a stage prefetch) joins back
+ * launch beside x1 -> x3, the stage-1 x2 / x3 exchanges beside the stage-2
+ * x1 flux launch, host<->device copies, a stage prefetch) joins back
  * to it before the call's later work, so events on it bracket all of it. */
 void* pmhd_gpu_stream(const pmhd_ctx* ctx);
 
