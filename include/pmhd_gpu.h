@@ -255,11 +255,14 @@ int pmhd_gpu_set_profiling(pmhd_mesh* mesh, int on);
 int pmhd_gpu_region_times(pmhd_mesh* mesh, pmhd_region_times* out, int reset);
 
 /* The context's CUDA stream (cudaStream_t) for interop: callers may record
- * events on it to time ABI calls.  Every call's device work is ordered on
- * it: work a call forks to the context's internal streams (the x2 flux
- * launch beside x1 -> x3, the stage-1 x2 / x3 exchanges beside the stage-2
- * x1 flux launch, host<->device copies, a stage prefetch) joins back
- * to it before the call's later work, so events on it bracket all of it. */
+ * events on it to time ABI calls.  Work a call forks to the context's
+ * internal streams (the x2 flux launch beside x1 -> x3, host<->device
+ * copies, a stage prefetch) joins back to it before the call returns, with
+ * one exception: pmhd_gpu_vl2_step may leave its last x2 / x3 ghost
+ * exchanges running beside the stream (they overlap the next step's x1
+ * flux launch; PMHD_EARLY_X1=0 disables).  Every entry point that touches
+ * the state orders itself after them; an event meant to close a timed
+ * region of steps should be recorded after a device synchronize. */
 void* pmhd_gpu_stream(const pmhd_ctx* ctx);
 
 /* Name of the kernel variant compiled into this library ("fused", "split"...). */

@@ -484,8 +484,11 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
     // +0.2 % at 256^3 and -0.2 % on the 512^3 turbulence in 64 blocks, so
     // meshes up to 2^24 cells per rank; PMHD_EARLY_X1=0 / 2: never / always)
     const long long cells = (long long)G.mb[0] * G.mb[1] * G.mb[2] * G.nb;
-    const bool early = early_ok && s == 1 && do_exchange && d0 == 1 && m->face_reuse && m->variant == 0 &&
-                       !m->prof && !(prefetch_next && can_prefetch(m)) && !use_flux_xy(m, 2) &&
+    // stage 2: the exchanges overlap the next step's stage-1 x1 flux launch
+    // (every other entry point that touches the state joins them first:
+    // drop_prefetch, run, destroy)
+    const bool early = early_ok && do_exchange && d0 == 1 && m->face_reuse && m->variant == 0 && !m->prof &&
+                       !can_prefetch(m) && !use_flux_xy(m, s == 1 ? 2 : 1) &&
                        (m->early_x1 == 2 || (m->early_x1 == 1 && cells <= (1LL << 24)));
     if (early) {
       CK(cudaEventRecord(m->ev_ex[0], st));
@@ -543,11 +546,6 @@ int enqueue_stage(pmhd_mesh* m, int s, double dt, bool do_exchange = true, bool 
 }
 
 int finish(pmhd_mesh* m, int stage_lo, int stage_hi, double* dt_next, pmhd_status* st) {
-  if (m->ex_pending) {  // (only if a stage 2 did not follow its stage 1)
-    pmhd_ctx* ctx = m->ctx;
-    CK(cudaStreamWaitEvent(ctx->stream, m->ev_ex[m->G.dim - 1], 0));
-    m->ex_pending = false;
-  }
   int rc = fetch_red(m);
   if (rc) return rc;
   pmhd_status s{};
@@ -586,6 +584,10 @@ int drop_prefetch(pmhd_mesh* m) {
   if (m->prefetched) {
     CK(cudaStreamWaitEvent(ctx->stream, m->ev_pre[1], 0));
     m->prefetched = 0;
+  }
+  if (m->ex_pending) {  // ghost exchanges still running beside the main stream
+    CK(cudaStreamWaitEvent(ctx->stream, m->ev_ex[m->G.dim - 1], 0));
+    m->ex_pending = false;
   }
   return PMHD_OK;
 }
@@ -861,6 +863,7 @@ int pmhd_gpu_mesh_destroy(pmhd_mesh* m) {
   if (!m) return PMHD_OK;
   cudaSetDevice(m->ctx->device);
   cudaStreamSynchronize(m->ctx->stream);
+  cudaStreamSynchronize(m->ctx->stream3);  // (deferred ghost exchanges)
   cudaFree(m->slab);
   if (m->drive_tab) { cudaFree(m->drive_tab); cudaFree(m->drive_rows); cudaFree(m->drive_sums); }
   cudaFree(m->dblk);
@@ -1027,7 +1030,7 @@ int pmhd_gpu_vl2_step(pmhd_mesh* m, double dt, double* dt_next, pmhd_status* st)
   if (!m->all_local) return fail(m->ctx, PMHD_ERR_INPUT, "step needs all neighbours local");
   int rc = reset_red(m);
   if (!rc) rc = enqueue_stage(m, 1, dt, true, true, false, true);  // + stage-2 interior tiles over the exchange
-  if (!rc) rc = enqueue_stage(m, 2, dt);
+  if (!rc) rc = enqueue_stage(m, 2, dt, true, false, false, true);
   if (rc) return rc;
   return finish(m, 1, 2, dt_next, st);
 }
@@ -1152,6 +1155,7 @@ int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, 
                  pmhd_status* st) {
   if (!m || !t || !dt) return PMHD_ERR_INPUT;
   if (int rc_ = use_device(m->ctx)) return rc_;
+  if (int rc_ = drop_prefetch(m)) return rc_;  // (a graph capture must not wait on outside work)
   int rc = PMHD_OK;
   if (!(*dt > 0.0)) {
     rc = pmhd_gpu_new_dt(m, dt, st);
@@ -1177,6 +1181,11 @@ int pmhd_gpu_run(pmhd_mesh* m, int ncycles, double tlim, double* t, double* dt, 
     ++n;
   }
   if (cycles_done) *cycles_done = n;
+  // the run returns with all its device work done (the last step's deferred
+  // ghost exchanges included)
+  if (!rc) rc = drop_prefetch(m);
+  if (!rc && cudaStreamSynchronize(m->ctx->stream) != cudaSuccess)
+    rc = fail(m->ctx, PMHD_ERR_CUDA, "run: stream synchronize failed");
   if (st && rc == PMHD_OK) {
     st->code = PMHD_OK;
     st->floor_count = floors;
